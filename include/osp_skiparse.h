@@ -1,0 +1,160 @@
+/*
+ * osp_skiparse.h -- C ABI of the B200-native Skiparse-2D Attention hot path.
+ *
+ * The reference (arxiv 2605.28691 "OSP-Next", package `osp`, pure Python/numpy) has no FFI;
+ * its hot-path entry points are Python functions.  Each function below is the device-side
+ * replacement of one of them and cites the reference interface it replaces
+ * (path:line under /root/reference/pkg/src/osp/).  The Python shim
+ * `paper_2605_28691_b200` binds these with ctypes and keeps the reference names and
+ * signatures.
+ *
+ * Conventions
+ *   - All pointers are device pointers; buffers are caller-owned; nothing is allocated.
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy default) and
+ *     never synchronises the host.
+ *   - Tensors are dense (batch, seq, chan) row-major unless a row stride (in elements) is
+ *     given.  Rearranges move whole channel vectors of `chan * elem_bytes` bytes and are
+ *     dtype-agnostic (1/2/4/8-byte elements, bit-exact).
+ *   - Return value: OSP_OK or an OSP_E_* code; osp_last_error() gives a thread-local message.
+ *     Codes map 1:1 onto the reference's exception classes.
+ *   - Re-entrant; the only global state is a once-per-kernel shared-memory attribute.
+ */
+#ifndef OSP_SKIPARSE_H_
+#define OSP_SKIPARSE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OSP_ABI_VERSION 1
+
+enum osp_status {
+  OSP_OK = 0,
+  OSP_E_PATTERN = 1,     /* skiparse.PatternError   skiparse.py:33-34 */
+  OSP_E_SHAPE = 2,       /* gridseq.ShapeError      gridseq.py:37 */
+  OSP_E_COORDINATE = 3,  /* gridseq.CoordinateError gridseq.py:33 */
+  OSP_E_SHARDING = 4,    /* ssp.ShardingError       ssp.py:33 */
+  OSP_E_COLLECTIVE = 5,  /* ssp.CollectiveError     ssp.py:37 */
+  OSP_E_PROTOCOL = 6,    /* ssp.ProtocolError       ssp.py:41 */
+  OSP_E_VALUE = 7,       /* ValueError (bad argument) */
+  OSP_E_UNSUPPORTED = 8, /* dtype / head_dim outside the B200 kernels' support */
+  OSP_E_CUDA = 9         /* CUDA runtime / driver failure -> RuntimeError */
+};
+
+/* Map ids: the six maps of skiparse.py:68-140 plus pad / strip (anyres.py:69-89). */
+enum osp_map_id {
+  OSP_MAP_IDENTITY = 0, /* IndexMap.identity            gridseq.py:192-195 */
+  OSP_MAP_O2T = 1,      /* orig_to_tsa                  skiparse.py:68-77  */
+  OSP_MAP_T2O = 2,      /* tsa_to_orig                  skiparse.py:80-88  */
+  OSP_MAP_O2G = 3,      /* orig_to_gsa                  skiparse.py:91-102 */
+  OSP_MAP_G2O = 4,      /* gsa_to_orig                  skiparse.py:105-114 */
+  OSP_MAP_T2G = 5,      /* tsa_to_gsa                   skiparse.py:117-128 */
+  OSP_MAP_G2T = 6,      /* gsa_to_tsa                   skiparse.py:131-140 */
+  OSP_MAP_PAD = 7,      /* pad_tensor (zero pad)        anyres.py:69-82    */
+  OSP_MAP_STRIP = 8     /* strip_padding                anyres.py:85-89    */
+};
+
+enum osp_pattern { OSP_PATTERN_ORIGINAL = 0, OSP_PATTERN_TSA = 1, OSP_PATTERN_GSA = 2 };
+
+const char* osp_last_error(void);
+int osp_abi_version(void);
+/* OSP_OK iff the current device is a Blackwell sm_100 part the kernels were built for. */
+int osp_device_check(void);
+
+/*
+ * K1: Skiparse Rearrange.  Replaces IndexMap.apply (gridseq.py:161-169) of the maps built by
+ * skiparse.py:68-140 (and pad_tensor / strip_padding, anyres.py:69-89).
+ * (t, h, w, k) is the PADDED grid.  h_orig/w_orig (<= h/w; 0 = same as h/w) are the original
+ * extents: O2T/O2G then read the UNPADDED original tensor and write zero pad slots (fused
+ * pad_tensor), T2O/G2O write the UNPADDED original tensor (fused strip_padding).
+ * T2G/G2T/IDENTITY require h_orig == h, w_orig == w.
+ * Divisibility is checked exactly as skiparse.py:53-65 (OSP_E_PATTERN).
+ */
+int osp_rearrange(const void* src, void* dst, int64_t elem_bytes, int64_t chan, int64_t batch,
+                  int64_t t, int64_t h, int64_t w, int64_t k, int map_id, int64_t h_orig,
+                  int64_t w_orig, void* stream);
+
+/* Table-driven gather for arbitrary IndexMaps (gridseq.py:161-169):
+ * dst[i] = src[index[i]] over rows of row_bytes; index entries outside [0, n_in_rows) give
+ * zero rows (the Python shim validates tables as gridseq.py:140-150 does). */
+int osp_gather_rows(const void* src, void* dst, const int64_t* index, int64_t n_out_rows,
+                    int64_t n_in_rows, int64_t row_bytes, void* stream);
+/* IndexMap.invert (gridseq.py:179-185): inv[index[i]] = i. */
+int osp_invert_index(const int64_t* index, int64_t* inv, int64_t n, void* stream);
+
+/*
+ * K5: 1-D validity masks as bit words, bits[row * ceil(L/32) + pos/32] bit (pos%32).
+ * osp_pattern_mask_bits: subsequence_mask (anyres.py:92-96) for `batch` items in the enlarged
+ * batch order (pattern id, batch item) of attention.py:121-125; pattern ORIGINAL gives the
+ * flat padded-grid mask (anyres.py:61-64) per batch item.  (t,h,w,k) padded, h_orig/w_orig
+ * original extents.
+ */
+int osp_pattern_mask_bits(uint32_t* bits, int64_t batch, int64_t t, int64_t h, int64_t w,
+                          int64_t k, int pattern, int64_t h_orig, int64_t w_orig, void* stream);
+int osp_mask_bytes_to_bits(const uint8_t* valid, uint32_t* bits, int64_t n_rows, int64_t len,
+                           void* stream);
+int osp_mask_bits_to_bytes(const uint32_t* bits, uint8_t* valid, int64_t n_rows, int64_t len,
+                           void* stream);
+
+/*
+ * K2: per-subsequence attention forward.  Replaces dense_attention (attention.py:47-67) as
+ * called per subsequence by skiparse_attention (attention.py:126-130), extended to `heads`
+ * heads of `head_dim` channels each (head_dim in {64, 128}; bf16 in/out, fp32 accumulate).
+ *   q,k,v,o : (n_seq, seq_len, >= heads*head_dim) bf16 with row strides q_stride.. (elements)
+ *   lse     : (n_seq, heads, seq_len) fp32 natural-log softmax normaliser; +inf for rows with
+ *             no valid key or (zero_invalid_queries) an invalid query.
+ *   valid_bits: NULL or (n_seq, ceil(seq_len/32)) key validity (attention.py:35-44 rules:
+ *             masked keys weigh 0, an all-masked row outputs 0).
+ *   zero_invalid_queries: rows whose own bit is 0 output 0 (attention.py:127-130).
+ *   scale   : softmax scale (reference: 1/sqrt(chan) with one head, attention.py:57).
+ */
+int osp_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n_seq,
+                 int64_t seq_len, int64_t heads, int64_t head_dim, int64_t q_stride,
+                 int64_t k_stride, int64_t v_stride, int64_t o_stride, const uint32_t* valid_bits,
+                 int zero_invalid_queries, float scale, void* stream);
+
+/*
+ * K3: backward of osp_attn_fwd (no reference counterpart: attention.py has no backward).
+ * Writes dq, dk, dv (bf16, own row strides).  workspace >= osp_attn_bwd_workspace_bytes().
+ */
+size_t osp_attn_bwd_workspace_bytes(int64_t n_seq, int64_t seq_len, int64_t heads,
+                                    int64_t head_dim);
+int osp_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                 const float* lse, void* dq, void* dk, void* dv, int64_t n_seq, int64_t seq_len,
+                 int64_t heads, int64_t head_dim, int64_t q_stride, int64_t k_stride,
+                 int64_t v_stride, int64_t o_stride, int64_t do_stride, int64_t dq_stride,
+                 int64_t dk_stride, int64_t dv_stride, const uint32_t* valid_bits,
+                 int zero_invalid_queries, float scale, void* workspace, size_t workspace_bytes,
+                 void* stream);
+
+/*
+ * K4: Sparse Sequence Parallel pattern switch, local steps of ssp_pattern_switch
+ * (ssp.py:139-180; Alg. 1).  One rank's shard is (local_batch, L, chan) with
+ * L = t*h*w/k^2, local_batch = G*b, G = k^2/group_size; (t,h,w,k) the padded global grid.
+ *   osp_ssp_pack:   step 1 (ssp.py:166): orig_to_tsa on the reduced grid (t, h/k, w/k) with
+ *                   batch G*b -> send buffer (k^2*G*b, L/k^2, chan) = group_size equal chunks.
+ *   osp_ssp_unpack: steps 3+4 (ssp.py:172-178): view the received buffer as
+ *                   (N, G, G, b, L/k^2, chan), swap axes 1 and 2, tsa_to_orig on the reduced
+ *                   grid -> (G*b, L, chan) in the switched pattern layout.
+ * Step 2 is one all-to-all of equal chunks (ssp.py:168), done by NCCL between the two.
+ * Errors: OSP_E_SHARDING (k^2 % group_size), OSP_E_PROTOCOL (local_batch % G), as ssp.py:145-160.
+ */
+int osp_ssp_pack(const void* src, void* dst, int64_t elem_bytes, int64_t chan,
+                 int64_t group_size, int64_t local_batch, int64_t t, int64_t h, int64_t w,
+                 int64_t k, void* stream);
+int osp_ssp_unpack(const void* recv, void* dst, int64_t elem_bytes, int64_t chan,
+                   int64_t group_size, int64_t local_batch, int64_t t, int64_t h, int64_t w,
+                   int64_t k, void* stream);
+
+/* Self-test of the tcgen05 instruction forms (S = A B^T, O = bf16(S) V for one 128-row tile). */
+int osp_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,
+                  int64_t head_dim, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OSP_SKIPARSE_H_ */

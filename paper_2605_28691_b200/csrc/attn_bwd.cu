@@ -1,0 +1,541 @@
+// K3: backward of the per-subsequence attention (no reference counterpart: the reference
+// attention.py has no backward; semantics follow the forward's exact-zero rules, so masked
+// keys, pad queries and key-less rows get zero gradient).
+//
+// Three launches:
+//   1. prep     : delta[q] = sum_c dO[q,c] O[q,c] (fp32), lse2 = lse*log2(e) (+inf kept),
+//                 both padded to a multiple of 128 queries (+inf / 0), dq accumulator zeroed.
+//   2. main     : one CTA per (128-key tile, head, subsequence) streams all 128-query tiles.
+//                 Transposed scores so a thread owns a key row:
+//                   S^T = K Q^T, dP^T = V dO^T            (SS MMAs into TMEM)
+//                   P^T = exp2(S^T*c - lse2), dS^T = P^T (dP^T - delta)   (compute warps)
+//                   dV += P^T dO   (P^T read from TMEM),  dK += dS^T Q,  dQ_i = dS K
+//                 dV/dK accumulate in TMEM across the whole loop; dQ_i is drained from TMEM by
+//                 four writer warps with fp32 vector atomics into the workspace.
+//                 TMEM: [0,128) S^T/P^T, [128,256) dP^T then dQ_i, [256,256+D) dV,
+//                 [256+D, 256+2D) dK.
+//   3. finalize : dq = bf16(scale * dq_acc).
+#include "osp_common.cuh"
+#include "osp_internal.h"
+
+namespace osp {
+namespace {
+
+constexpr int kBwdThreads = 384;
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <int D>
+struct BwdLayout {
+  static constexpr int kTile = 128 * D * 2;
+  static constexpr int kK = 0;
+  static constexpr int kV = kK + kTile;
+  static constexpr int kQ = kV + kTile;            // 2 stages
+  static constexpr int kDO = kQ + 2 * kTile;       // 2 stages
+  static constexpr int kDS = kDO + 2 * kTile;      // 128 keys x 128 queries bf16 = 32 KB
+  static constexpr int kStat = kDS + 32768;        // 2 stages x (lse2[128], delta[128]) fp32
+  static constexpr int kBar = kStat + 2 * 1024;
+  static constexpr int kSmem = kBar + 256;
+};
+
+struct BwdArgs {
+  const float* lse2;    // (n_seq, heads, Lp)
+  const float* delta;   // (n_seq, heads, Lp)
+  float* dq_acc;        // (n_seq, L, heads, D)
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  int64_t dk_stride, dv_stride;
+  const uint32_t* valid_bits;
+  int words_per_seq;
+  int seq_len, seq_pad, heads, n_q;
+  float scale, scale_log2;
+};
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                    const BwdArgs a) {
+  using Ly = BwdLayout<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Ly::kBar);
+  uint64_t* bar_kv = bars + 0;
+  uint64_t* bar_qf = bars + 1;    // [2] Q, dO, lse2, delta of a stage landed
+  uint64_t* bar_qe = bars + 3;    // [2] stage free
+  uint64_t* bar_s = bars + 5;     // S^T ready
+  uint64_t* bar_dp = bars + 6;    // dP^T ready
+  uint64_t* bar_p = bars + 7;     // P^T written (128 arrivals)
+  uint64_t* bar_ds = bars + 8;    // dS^T written (128 arrivals)
+  uint64_t* bar_dsf = bars + 9;   // dS smem free again
+  uint64_t* bar_dq = bars + 10;   // dQ_i ready in TMEM
+  uint64_t* bar_dqf = bars + 11;  // dQ_i drained (128 arrivals)
+  uint64_t* bar_fin = bars + 12;  // dK, dV final
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int head = blockIdx.y;
+  const int seq = blockIdx.z;
+  const int kv0 = blockIdx.x * 128;
+
+  if ((smem_u32(sm) & 1023) != 0) __trap();
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_kv, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_qf + i, 1);
+      mbar_init(bar_qe + i, 1);
+    }
+    mbar_init(bar_s, 1);
+    mbar_init(bar_dp, 1);
+    mbar_init(bar_p, 128);
+    mbar_init(bar_ds, 128);
+    mbar_init(bar_dsf, 1);
+    mbar_init(bar_dq, 1);
+    mbar_init(bar_dqf, 128);
+    mbar_init(bar_fin, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tA = tmem, tB = tmem + 128, tDV = tmem + 256, tDK = tmem + 256 + D;
+
+  const float* lse2_g = a.lse2 + (static_cast<int64_t>(seq) * a.heads + head) * a.seq_pad;
+  const float* delta_g = a.delta + (static_cast<int64_t>(seq) * a.heads + head) * a.seq_pad;
+
+  if (warp < 4) {
+    regs_dec<56>();
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      tma_prefetch(&tmDO);
+      mbar_expect_tx(bar_kv, 2 * Ly::kTile);
+#pragma unroll
+      for (int s = 0; s < D / 64; ++s) {
+        tma_load_3d(sm + Ly::kK + s * 16384, &tmK, bar_kv, head * D + s * 64, kv0, seq);
+        tma_load_3d(sm + Ly::kV + s * 16384, &tmV, bar_kv, head * D + s * 64, kv0, seq);
+      }
+      for (int i = 0; i < a.n_q; ++i) {
+        const int st = i & 1;
+        mbar_wait(bar_qe + st, ((i >> 1) & 1) ^ 1);
+        mbar_expect_tx(bar_qf + st, 2 * Ly::kTile + 1024);
+#pragma unroll
+        for (int s = 0; s < D / 64; ++s) {
+          tma_load_3d(sm + Ly::kQ + st * Ly::kTile + s * 16384, &tmQ, bar_qf + st,
+                      head * D + s * 64, i * 128, seq);
+          tma_load_3d(sm + Ly::kDO + st * Ly::kTile + s * 16384, &tmDO, bar_qf + st,
+                      head * D + s * 64, i * 128, seq);
+        }
+        bulk_load(sm + Ly::kStat + st * 1024, lse2_g + i * 128, 512, bar_qf + st);
+        bulk_load(sm + Ly::kStat + st * 1024 + 512, delta_g + i * 128, 512, bar_qf + st);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t kIdSS = idesc_bf16(128, 128, 0, 0);   // S^T, dP^T
+      constexpr uint32_t kIdKmn = idesc_bf16(128, D, 0, 1);    // dV (TS), dK
+      constexpr uint32_t kIdMNmn = idesc_bf16(128, D, 1, 1);   // dQ
+      const uint32_t k_base = smem_u32(sm + Ly::kK);
+      const uint32_t v_base = smem_u32(sm + Ly::kV);
+      const uint32_t ds_base = smem_u32(sm + Ly::kDS);
+      mbar_wait(bar_kv, 0);
+      for (int i = 0; i < a.n_q; ++i) {
+        const int st = i & 1;
+        const uint32_t q_base = smem_u32(sm + Ly::kQ + st * Ly::kTile);
+        const uint32_t do_base = smem_u32(sm + Ly::kDO + st * Ly::kTile);
+        mbar_wait(bar_qf + st, (i >> 1) & 1);
+        tc_fence_after();
+        // S^T = K Q^T  -> tA
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tA, sdesc_sw128(k_base + off, 16, 1024), sdesc_sw128(q_base + off, 16, 1024), kIdSS,
+                 kk > 0);
+        }
+        tc_commit(bar_s);
+        // dP^T = V dO^T -> tB (after the previous dQ was drained)
+        if (i > 0) {
+          mbar_wait(bar_dqf, (i - 1) & 1);
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tB, sdesc_sw128(v_base + off, 16, 1024), sdesc_sw128(do_base + off, 16, 1024), kIdSS,
+                 kk > 0);
+        }
+        tc_commit(bar_dp);
+        // dV += P^T dO   (A = P^T from TMEM)
+        mbar_wait(bar_p, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tDV, tA + kk * 8, sdesc_sw128(do_base + kk * 2048, 16384, 1024), kIdKmn,
+                 (i > 0 || kk > 0) ? 1u : 0u);
+        // dK += dS^T Q   (A = dS^T, K-major in smem)
+        mbar_wait(bar_ds, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tDK, sdesc_sw128(ds_base + off, 16, 1024), sdesc_sw128(q_base + kk * 2048, 16384, 1024),
+                 kIdKmn, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(bar_qe + st);
+        // dQ_i = dS K  -> tB   (A = dS, M(query)-major view of the same smem buffer)
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ss(tB, sdesc_sw128(ds_base + kk * 2048, 16384, 1024),
+                 sdesc_sw128(k_base + kk * 2048, 16384, 1024), kIdMNmn, kk > 0);
+        tc_commit(bar_dq);
+        tc_commit(bar_dsf);
+      }
+      tc_commit(bar_fin);
+    }
+  }
+  } else if (warp < 8) {
+    regs_inc<232>();
+    // -------------------------------------------------------------- compute warps (key rows)
+    const int wq = warp & 3;
+    const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
+    const int krow = wq * 32 + lane;  // key row within the tile
+    const int kglob = kv0 + krow;
+    bool kvalid = kglob < a.seq_len;
+    if (kvalid && a.valid_bits) {
+      const uint32_t* vb = a.valid_bits + static_cast<int64_t>(seq) * a.words_per_seq;
+      kvalid = (__ldg(vb + (kglob >> 5)) >> (kglob & 31)) & 1u;
+    }
+    const float c = a.scale_log2;
+    uint8_t* ds_row0 = sm + Ly::kDS + krow * 128;
+    for (int i = 0; i < a.n_q; ++i) {
+      const int st = i & 1;
+      const float* lse_s = reinterpret_cast<const float*>(sm + Ly::kStat + st * 1024);
+      const float* del_s = lse_s + 128;
+      mbar_wait(bar_qf + st, (i >> 1) & 1);  // lse2 / delta of this stage landed
+      mbar_wait(bar_s, i & 1);
+      tc_fence_after();
+      float p[128];
+      {
+        uint32_t s[4][32];
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) tmem_ld32(tA + lane_addr + cc * 32, s[cc]);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) tmem_wait_ld(s[cc]);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+#pragma unroll
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float4 l4 = *reinterpret_cast<const float4*>(lse_s + cc * 32 + i4 * 4);
+            p[cc * 32 + i4 * 4 + 0] = ex2(fmaf(__uint_as_float(s[cc][i4 * 4 + 0]), c, -l4.x));
+            p[cc * 32 + i4 * 4 + 1] = ex2(fmaf(__uint_as_float(s[cc][i4 * 4 + 1]), c, -l4.y));
+            p[cc * 32 + i4 * 4 + 2] = ex2(fmaf(__uint_as_float(s[cc][i4 * 4 + 2]), c, -l4.z));
+            p[cc * 32 + i4 * 4 + 3] = ex2(fmaf(__uint_as_float(s[cc][i4 * 4 + 3]), c, -l4.w));
+          }
+        }
+      }
+      if (!kvalid) {
+#pragma unroll
+        for (int j = 0; j < 128; ++j) p[j] = 0.f;
+      }
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(p[cc * 32 + 2 * j], p[cc * 32 + 2 * j + 1]);
+        tmem_st16(tA + lane_addr + cc * 16, pk);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar_p);
+
+      mbar_wait(bar_dp, i & 1);
+      tc_fence_after();
+      if (i > 0) mbar_wait(bar_dsf, (i - 1) & 1);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t dp[32];
+        tmem_ld32(tB + lane_addr + cc * 32, dp);
+        tmem_wait_ld(dp);
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float d0 = del_s[cc * 32 + 2 * j], d1 = del_s[cc * 32 + 2 * j + 1];
+          const float ds0 = p[cc * 32 + 2 * j] * (__uint_as_float(dp[2 * j]) - d0);
+          const float ds1 = p[cc * 32 + 2 * j + 1] * (__uint_as_float(dp[2 * j + 1]) - d1);
+          pk[j] = pack_bf16(ds0, ds1);
+        }
+        // queries cc*32 .. cc*32+31 = 4 16-byte chunks of sub-tile cc/2, chunk base (cc&1)*4
+        uint8_t* sub = ds_row0 + (cc >> 1) * 16384;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          const int logical = (cc & 1) * 4 + ch;
+          const int phys = logical ^ (krow & 7);
+          *reinterpret_cast<uint4*>(sub + phys * 16) =
+              make_uint4(pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(bar_ds);
+    }
+    // ---------------------------------------------------------------- dK / dV epilogue
+    mbar_wait(bar_fin, 0);
+    tc_fence_after();
+    const bool row_ok = kglob < a.seq_len;
+    __nv_bfloat16* dvrow = a.dv + (static_cast<int64_t>(seq) * a.seq_len + kglob) * a.dv_stride +
+                           static_cast<int64_t>(head) * D;
+    __nv_bfloat16* dkrow = a.dk + (static_cast<int64_t>(seq) * a.seq_len + kglob) * a.dk_stride +
+                           static_cast<int64_t>(head) * D;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t base = (which == 0 ? tDV : tDK) + lane_addr;
+      const float mul = which == 0 ? 1.f : a.scale;
+      __nv_bfloat16* row = which == 0 ? dvrow : dkrow;
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t o[32];
+        tmem_ld32(base + cc * 32, o);
+        tmem_wait_ld(o);
+        if (row_ok) {
+          uint4 pk[4];
+          uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            pw[j] = pack_bf16(__uint_as_float(o[2 * j]) * mul, __uint_as_float(o[2 * j + 1]) * mul);
+          uint4* dst = reinterpret_cast<uint4*>(row + cc * 32);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dst[j] = pk[j];
+        }
+      }
+    }
+  } else {
+    regs_dec<152>();
+    // -------------------------------------------------------------- dQ writer warps
+    const int wq = warp & 3;
+    const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
+    const int qrow = wq * 32 + lane;
+    for (int i = 0; i < a.n_q; ++i) {
+      mbar_wait(bar_dq, i & 1);
+      tc_fence_after();
+      const int qg = i * 128 + qrow;
+      float* dst = a.dq_acc + ((static_cast<int64_t>(seq) * a.seq_len + qg) * a.heads + head) * D;
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tB + lane_addr + cc * 32, v);
+        tmem_wait_ld(v);
+        if (cc == D / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(bar_dqf);
+        }
+        if (qg < a.seq_len) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            red_add_v4(dst + cc * 32 + j * 4, __uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                       __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// delta and log2-domain lse per (seq, head, query), padded to seq_pad; one warp per row.
+template <int D>
+__global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t o_stride,
+                                const __nv_bfloat16* __restrict__ dout, int64_t do_stride,
+                                const float* __restrict__ lse, float* lse2, float* delta, int64_t n_seq,
+                                int heads, int seq_len, int seq_pad) {
+  const int64_t total = n_seq * heads * static_cast<int64_t>(seq_pad);
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total;
+       w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int q = static_cast<int>(w % seq_pad);
+    const int64_t sh = w / seq_pad;
+    const int h = static_cast<int>(sh % heads);
+    const int64_t s = sh / heads;
+    float acc = 0.f;
+    if (q < seq_len) {
+      const __nv_bfloat16* orow = o + (s * seq_len + q) * o_stride + static_cast<int64_t>(h) * D;
+      const __nv_bfloat16* drow = dout + (s * seq_len + q) * do_stride + static_cast<int64_t>(h) * D;
+      for (int c = lane * 2; c < D; c += 64) {
+        const float2 of = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(orow + c));
+        const float2 df = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(drow + c));
+        acc += of.x * df.x + of.y * df.y;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, off);
+    if (lane == 0) {
+      delta[w] = acc;
+      lse2[w] = q < seq_len ? lse[sh * seq_len + q] * kLog2e : INFINITY;
+    }
+  }
+}
+
+template <int D>
+__global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16* dq, int64_t dq_stride,
+                                   int64_t rows, int heads, float scale) {
+  const int64_t per_row = static_cast<int64_t>(heads) * D / 4;
+  const int64_t total = rows * per_row;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / per_row, c4 = i - r * per_row;
+    const float4 v = reinterpret_cast<const float4*>(acc)[i];
+    uint2 pk;
+    pk.x = pack_bf16(v.x * scale, v.y * scale);
+    pk.y = pack_bf16(v.z * scale, v.w * scale);
+    *reinterpret_cast<uint2*>(dq + r * dq_stride + c4 * 4) = pk;
+  }
+}
+
+struct BwdWs {
+  float* dq_acc;
+  float* lse2;
+  float* delta;
+};
+
+BwdWs carve(void* ws, const AttnShape& s) {
+  const int64_t seq_pad = (s.seq_len + 127) / 128 * 128;
+  BwdWs w;
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  w.dq_acc = reinterpret_cast<float*>(p);
+  p += ((s.n_seq * s.seq_len * s.heads * s.head_dim * 4 + 255) / 256) * 256;
+  w.lse2 = reinterpret_cast<float*>(p);
+  p += ((s.n_seq * s.heads * seq_pad * 4 + 255) / 256) * 256;
+  w.delta = reinterpret_cast<float*>(p);
+  return w;
+}
+
+unsigned grid_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > 148 * 32) b = 148 * 32;
+  if (b < 1) b = 1;
+  return static_cast<unsigned>(b);
+}
+
+template <int D>
+int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                 const float* lse, void* dq, void* dk, void* dv, const AttnShape& s, int64_t qs,
+                 int64_t ks, int64_t vs, int64_t os, int64_t dos, int64_t dqs, int64_t dks,
+                 int64_t dvs, const uint32_t* bits, float scale, void* workspace, cudaStream_t stream) {
+  const int64_t seq_pad = (s.seq_len + 127) / 128 * 128;
+  BwdWs w = carve(workspace, s);
+  int rc = check_cuda(cudaMemsetAsync(w.dq_acc, 0, s.n_seq * s.seq_len * s.heads * D * 4, stream),
+                      "memset dq_acc");
+  if (rc != kOk) return rc;
+  {
+    const int64_t rows = s.n_seq * s.heads * seq_pad;
+    bwd_prep_kernel<D><<<grid_for(rows * 32, 256), 256, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(o), os, static_cast<const __nv_bfloat16*>(dout), dos, lse,
+        w.lse2, w.delta, s.n_seq, static_cast<int>(s.heads), static_cast<int>(s.seq_len),
+        static_cast<int>(seq_pad));
+    rc = check_cuda(cudaGetLastError(), "bwd_prep launch");
+    if (rc != kOk) return rc;
+  }
+  CUtensorMap mq, mk, mv, mdo;
+  const int64_t cols = s.heads * D;
+  if ((rc = make_tmap_bf16_3d(&mq, q, cols, s.seq_len, s.n_seq, qs, 128)) != kOk) return rc;
+  if ((rc = make_tmap_bf16_3d(&mk, k, cols, s.seq_len, s.n_seq, ks, 128)) != kOk) return rc;
+  if ((rc = make_tmap_bf16_3d(&mv, v, cols, s.seq_len, s.n_seq, vs, 128)) != kOk) return rc;
+  if ((rc = make_tmap_bf16_3d(&mdo, dout, cols, s.seq_len, s.n_seq, dos, 128)) != kOk) return rc;
+  if ((dks * 2) % 16 || (dvs * 2) % 16 || (reinterpret_cast<uintptr_t>(dk) & 15) ||
+      (reinterpret_cast<uintptr_t>(dv) & 15) || (dqs * 2) % 8 || (reinterpret_cast<uintptr_t>(dq) & 7)) {
+    set_error("gradient outputs need 16-byte aligned bases/row strides");
+    return kValue;
+  }
+  BwdArgs a;
+  a.lse2 = w.lse2;
+  a.delta = w.delta;
+  a.dq_acc = w.dq_acc;
+  a.dk = static_cast<__nv_bfloat16*>(dk);
+  a.dv = static_cast<__nv_bfloat16*>(dv);
+  a.dk_stride = dks;
+  a.dv_stride = dvs;
+  a.valid_bits = bits;
+  a.words_per_seq = static_cast<int>((s.seq_len + 31) / 32);
+  a.seq_len = static_cast<int>(s.seq_len);
+  a.seq_pad = static_cast<int>(seq_pad);
+  a.heads = static_cast<int>(s.heads);
+  a.n_q = static_cast<int>(seq_pad / 128);
+  a.scale = scale;
+  a.scale_log2 = scale * kLog2e;
+  static bool attr_set = false;
+  if (!attr_set) {
+    rc = check_cuda(cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         BwdLayout<D>::kSmem),
+                    "cudaFuncSetAttribute(attn_bwd)");
+    if (rc != kOk) return rc;
+    attr_set = true;
+  }
+  dim3 grid(static_cast<unsigned>(seq_pad / 128), static_cast<unsigned>(s.heads),
+            static_cast<unsigned>(s.n_seq));
+  attn_bwd_kernel<D><<<grid, kBwdThreads, BwdLayout<D>::kSmem, stream>>>(mq, mk, mv, mdo, a);
+  rc = check_cuda(cudaGetLastError(), "attn_bwd_kernel launch");
+  if (rc != kOk) return rc;
+  const int64_t rows = s.n_seq * s.seq_len;
+  dq_finalize_kernel<D><<<grid_for(rows * s.heads * D / 4, 256), 256, 0, stream>>>(
+      w.dq_acc, static_cast<__nv_bfloat16*>(dq), dqs, rows, static_cast<int>(s.heads), scale);
+  return check_cuda(cudaGetLastError(), "dq_finalize launch");
+}
+
+}  // namespace
+
+size_t attn_bwd_workspace_bytes(const AttnShape& s) {
+  const int64_t seq_pad = (s.seq_len + 127) / 128 * 128;
+  const int64_t a = ((s.n_seq * s.seq_len * s.heads * s.head_dim * 4 + 255) / 256) * 256;
+  const int64_t b = ((s.n_seq * s.heads * seq_pad * 4 + 255) / 256) * 256;
+  return static_cast<size_t>(a + 2 * b);
+}
+
+int launch_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                    const float* lse, void* dq, void* dk, void* dv, const AttnShape& s,
+                    int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t o_stride,
+                    int64_t do_stride, int64_t dq_stride, int64_t dk_stride, int64_t dv_stride,
+                    const uint32_t* valid_bits, int zero_invalid_queries, float scale,
+                    void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+  (void)zero_invalid_queries;  // encoded in lse (+inf rows) by the forward
+  (void)workspace_bytes;
+  if (s.head_dim == 128)
+    return launch_bwd_t<128>(q, k, v, o, dout, lse, dq, dk, dv, s, q_stride, k_stride, v_stride,
+                             o_stride, do_stride, dq_stride, dk_stride, dv_stride, valid_bits, scale,
+                             workspace, stream);
+  if (s.head_dim == 64)
+    return launch_bwd_t<64>(q, k, v, o, dout, lse, dq, dk, dv, s, q_stride, k_stride, v_stride,
+                            o_stride, do_stride, dq_stride, dk_stride, dv_stride, valid_bits, scale,
+                            workspace, stream);
+  set_error("attention kernels support head_dim 64 or 128");
+  return kUnsupported;
+}
+
+}  // namespace osp

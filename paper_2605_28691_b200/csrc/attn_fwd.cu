@@ -1,0 +1,384 @@
+// K2: per-subsequence attention forward on sm_100a (tcgen05 + TMEM + TMA).
+//
+// Replaces the reference's dense_attention hot loop (attention.py:47-67) as called
+// per subsequence by skiparse_attention (attention.py:126): out = softmax(q k^T * scale +
+// key mask) v, with the reference's exact-zero rules (attention.py:35-44): masked keys weigh
+// 0, a row with no valid key outputs 0; optionally pad-query rows output 0
+// (attention.py:127-130).
+//
+// One CTA owns two 128-row query tiles of one (subsequence, head) and streams 128-key tiles.
+//   warp 0      TMA producer (Q once, K/V double-buffered, 128B-swizzled boxes of 64 cols)
+//   warp 1      MMA issuer   (single thread; S_t = Q_t K^T into TMEM, O_t += P_t V with P
+//                             read straight from TMEM)
+//   warp 2      TMEM allocator (512 columns: S0 | S1 | O0 | O1)
+//   warps 4-7   softmax for query tile 0, warps 8-11 for tile 1: one thread per row,
+//               online softmax in the log2 domain, lazy O rescaling (only when the running
+//               max grows by > 2^8), P written back into the S columns as packed bf16.
+// MMA order per key tile j: QK0_j, PV1_{j-1}, QK1_j, PV0_j, so one tile's softmax overlaps
+// the other tile's tensor-core work.
+#include "osp_common.cuh"
+#include "osp_internal.h"
+
+namespace osp {
+namespace {
+
+constexpr int kFwdThreads = 384;
+constexpr int kBM = 128;
+constexpr int kBN = 128;
+constexpr float kLn2 = 0.69314718055994530942f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+template <int D>
+struct FwdLayout {
+  static constexpr int kSub = D / 64;
+  static constexpr int kTile = kBM * D * 2;
+  static constexpr int kQ = 0;
+  static constexpr int kK = kQ + 2 * kTile;
+  static constexpr int kV = kK + 2 * kTile;
+  static constexpr int kBar = kV + 2 * kTile;
+  static constexpr int kSmem = kBar + 256 + 1024;
+};
+
+struct FwdArgs {
+  __nv_bfloat16* o;
+  int64_t o_stride;
+  float* lse;
+  const uint32_t* valid_bits;
+  int words_per_seq;
+  int seq_len;
+  int heads;
+  int n_kv;
+  float scale_log2;
+  int zero_invalid_q;
+};
+
+__device__ __forceinline__ bool bit_at(const uint32_t* bits, int words, int i) {
+  int w = i >> 5;
+  return w < words && ((__ldg(bits + w) >> (i & 31)) & 1u);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const FwdArgs a) {
+  using Ly = FwdLayout<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Ly::kBar);
+  uint64_t* bar_q = bars + 0;
+  uint64_t* bar_kf = bars + 2;
+  uint64_t* bar_ke = bars + 4;
+  uint64_t* bar_vf = bars + 6;
+  uint64_t* bar_ve = bars + 8;
+  uint64_t* bar_s = bars + 10;
+  uint64_t* bar_p = bars + 12;
+  uint64_t* bar_o = bars + 14;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int head = blockIdx.y;
+  const int seq = blockIdx.z;
+  const int q_row0 = blockIdx.x * 2 * kBM;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_q + i, 1);
+      mbar_init(bar_kf + i, 1);
+      mbar_init(bar_ke + i, 1);
+      mbar_init(bar_vf + i, 1);
+      mbar_init(bar_ve + i, 1);
+      mbar_init(bar_s + i, 1);
+      mbar_init(bar_p + i, 128);
+      mbar_init(bar_o + i, 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    regs_dec<56>();
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      for (int t = 0; t < 2; ++t) {
+        mbar_expect_tx(bar_q + t, Ly::kTile);
+#pragma unroll
+        for (int s = 0; s < Ly::kSub; ++s)
+          tma_load_3d(sm + Ly::kQ + t * Ly::kTile + s * 16384, &tmQ, bar_q + t, head * D + s * 64,
+                      q_row0 + t * kBM, seq);
+      }
+      for (int j = 0; j < a.n_kv; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(bar_ke + st, ph ^ 1);
+        mbar_expect_tx(bar_kf + st, Ly::kTile);
+#pragma unroll
+        for (int s = 0; s < Ly::kSub; ++s)
+          tma_load_3d(sm + Ly::kK + st * Ly::kTile + s * 16384, &tmK, bar_kf + st,
+                      head * D + s * 64, j * kBN, seq);
+        mbar_wait(bar_ve + st, ph ^ 1);
+        mbar_expect_tx(bar_vf + st, Ly::kTile);
+#pragma unroll
+        for (int s = 0; s < Ly::kSub; ++s)
+          tma_load_3d(sm + Ly::kV + st * Ly::kTile + s * 16384, &tmV, bar_vf + st,
+                      head * D + s * 64, j * kBN, seq);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t kIdQK = idesc_bf16(kBM, kBN, 0, 0);
+      constexpr uint32_t kIdPV = idesc_bf16(kBM, D, 0, 1);
+      const uint32_t q_base = smem_u32(sm + Ly::kQ);
+      const uint32_t k_base = smem_u32(sm + Ly::kK);
+      const uint32_t v_base = smem_u32(sm + Ly::kV);
+      auto qk = [&](int t, int st) {
+        const uint32_t qa = q_base + t * Ly::kTile;
+        const uint32_t kb = k_base + st * Ly::kTile;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tmem + t * 128, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
+                 kIdQK, kk > 0);
+        }
+      };
+      auto pv = [&](int t, int st, bool acc) {
+        const uint32_t vb = v_base + st * Ly::kTile;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                 sdesc_sw128(vb + kk * 2048, 16384, 1024), kIdPV, (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+      mbar_wait(bar_q + 0, 0);
+      mbar_wait(bar_q + 1, 0);
+      tc_fence_after();
+      for (int j = 0; j < a.n_kv; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(bar_kf + st, ph);
+        tc_fence_after();
+        qk(0, st);
+        tc_commit(bar_s + 0);
+        if (j > 0) {
+          mbar_wait(bar_p + 1, (j - 1) & 1);
+          tc_fence_after();
+          pv(1, (j - 1) & 1, j - 1 > 0);
+          tc_commit(bar_ve + ((j - 1) & 1));
+        }
+        qk(1, st);
+        tc_commit(bar_s + 1);
+        tc_commit(bar_ke + st);
+        mbar_wait(bar_vf + st, ph);
+        mbar_wait(bar_p + 0, j & 1);
+        tc_fence_after();
+        pv(0, st, j > 0);
+      }
+      const int last = a.n_kv - 1;
+      mbar_wait(bar_p + 1, last & 1);
+      tc_fence_after();
+      pv(1, last & 1, last > 0);
+      tc_commit(bar_ve + (last & 1));
+      tc_commit(bar_o + 0);
+      tc_commit(bar_o + 1);
+    }
+  }
+  } else {
+    regs_inc<224>();
+    // -------------------------------------------------------------- softmax / epilogue
+    const int t = (warp - 4) >> 2;
+    const int wq = warp & 3;
+    const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t tS = tmem + lane_addr + t * 128;
+    const uint32_t tO = tmem + lane_addr + 256 + t * 128;
+    const int q_row = q_row0 + t * kBM + wq * 32 + lane;
+    const uint32_t* vbits =
+        a.valid_bits ? a.valid_bits + static_cast<int64_t>(seq) * a.words_per_seq : nullptr;
+    const float c = a.scale_log2;
+
+    float m_used = -INFINITY;
+    float l = 0.f;
+    for (int j = 0; j < a.n_kv; ++j) {
+      mbar_wait(bar_s + t, j & 1);
+      tc_fence_after();
+      uint32_t s[4][32];
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) tmem_ld32(tS + cc * 32, s[cc]);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) tmem_wait_ld(s[cc]);
+
+      // key mask: validity bits and the subsequence tail
+      const int kv0 = j * kBN;
+      const int nvalid = min(kBN, a.seq_len - kv0);
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t m = vbits ? ((kv0 >> 5) + i < a.words_per_seq ? __ldg(vbits + (kv0 >> 5) + i) : 0u)
+                           : 0xFFFFFFFFu;
+        const int lo = i * 32;
+        if (nvalid <= lo) m = 0u;
+        else if (nvalid < lo + 32) m &= (1u << (nvalid - lo)) - 1u;
+        w[i] = m;
+      }
+      if ((w[0] & w[1] & w[2] & w[3]) != 0xFFFFFFFFu) {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (!((w[cc] >> i) & 1u)) s[cc][i] = __float_as_uint(-INFINITY);
+      }
+      float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        mx0 = fmaxf(mx0, __uint_as_float(s[0][i]));
+        mx1 = fmaxf(mx1, __uint_as_float(s[1][i]));
+        mx2 = fmaxf(mx2, __uint_as_float(s[2][i]));
+        mx3 = fmaxf(mx3, __uint_as_float(s[3][i]));
+      }
+      const float m_new = fmaxf(m_used, fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)));
+      const bool need = (m_new > m_used) &&
+                        (m_used == -INFINITY || (m_new - m_used) * c > kRescaleThreshold);
+      if (__any_sync(0xFFFFFFFFu, need)) {
+        const float m_upd = fmaxf(m_new, m_used);
+        const float alpha = (m_used == -INFINITY) ? 0.f : ex2((m_used - m_upd) * c);
+        if (j > 0) {
+#pragma unroll
+          for (int cc = 0; cc < D / 32; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(tO + cc * 32, o);
+            tmem_wait_ld(o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(tO + cc * 32, o);
+          }
+        }
+        l *= alpha;
+        m_used = m_upd;
+      }
+      const float ms = (m_used == -INFINITY) ? 0.f : m_used * c;
+      float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float p0 = ex2(fmaf(__uint_as_float(s[cc][2 * i]), c, -ms));
+          const float p1 = ex2(fmaf(__uint_as_float(s[cc][2 * i + 1]), c, -ms));
+          ls0 += p0;
+          ls1 += p1;
+          pk[i] = pack_bf16(p0, p1);
+        }
+        tmem_st16(tS + cc * 16, pk);
+      }
+      tmem_wait_st();
+      l += ls0 + ls1;
+      tc_fence_before();
+      mbar_arrive(bar_p + t);
+    }
+
+    // ---------------------------------------------------------------- epilogue
+    mbar_wait(bar_o + t, 0);
+    tc_fence_after();
+    const bool row_ok = q_row < a.seq_len;
+    bool q_valid = true;
+    if (a.zero_invalid_q && vbits && row_ok) q_valid = bit_at(vbits, a.words_per_seq, q_row);
+    const bool live = row_ok && q_valid && l > 0.f;
+    const float inv_l = live ? 1.f / l : 0.f;
+    __nv_bfloat16* orow = a.o + (static_cast<int64_t>(seq) * a.seq_len + q_row) * a.o_stride +
+                          static_cast<int64_t>(head) * D;
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld32(tO + cc * 32, o);
+      tmem_wait_ld(o);
+      if (row_ok) {
+        uint4 pk[4];
+        uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pw[i] = pack_bf16(__uint_as_float(o[2 * i]) * inv_l, __uint_as_float(o[2 * i + 1]) * inv_l);
+        uint4* dst = reinterpret_cast<uint4*>(orow + cc * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = pk[i];
+      }
+    }
+    if (row_ok) {
+      const float ms = (m_used == -INFINITY) ? 0.f : m_used * c;
+      a.lse[(static_cast<int64_t>(seq) * a.heads + head) * a.seq_len + q_row] =
+          live ? (ms + __log2f(l)) * kLn2 : INFINITY;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* lse,
+                 const AttnShape& s, int64_t qs, int64_t ks, int64_t vs, int64_t os,
+                 const uint32_t* bits, int zero_invalid_q, float scale, cudaStream_t stream) {
+  CUtensorMap mq, mk, mv;
+  const int64_t cols = s.heads * D;
+  int st;
+  if ((st = make_tmap_bf16_3d(&mq, q, cols, s.seq_len, s.n_seq, qs, kBM)) != kOk) return st;
+  if ((st = make_tmap_bf16_3d(&mk, k, cols, s.seq_len, s.n_seq, ks, kBN)) != kOk) return st;
+  if ((st = make_tmap_bf16_3d(&mv, v, cols, s.seq_len, s.n_seq, vs, kBN)) != kOk) return st;
+  FwdArgs a;
+  a.o = static_cast<__nv_bfloat16*>(o);
+  a.o_stride = os;
+  a.lse = lse;
+  a.valid_bits = bits;
+  a.words_per_seq = static_cast<int>((s.seq_len + 31) / 32);
+  a.seq_len = static_cast<int>(s.seq_len);
+  a.heads = static_cast<int>(s.heads);
+  a.n_kv = static_cast<int>((s.seq_len + kBN - 1) / kBN);
+  a.scale_log2 = scale * 1.4426950408889634f;
+  a.zero_invalid_q = zero_invalid_q;
+  const int n_qt = static_cast<int>((s.seq_len + kBM - 1) / kBM);
+  dim3 grid((n_qt + 1) / 2, static_cast<unsigned>(s.heads), static_cast<unsigned>(s.n_seq));
+  static bool attr_set = false;
+  if (!attr_set) {
+    int rc = check_cuda(cudaFuncSetAttribute(attn_fwd_kernel<D>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             FwdLayout<D>::kSmem),
+                        "cudaFuncSetAttribute(attn_fwd)");
+    if (rc != kOk) return rc;
+    attr_set = true;
+  }
+  attn_fwd_kernel<D><<<grid, kFwdThreads, FwdLayout<D>::kSmem, stream>>>(mq, mk, mv, a);
+  return check_cuda(cudaGetLastError(), "attn_fwd_kernel launch");
+}
+
+}  // namespace
+
+int launch_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                    const AttnShape& s, int64_t q_stride, int64_t k_stride, int64_t v_stride,
+                    int64_t o_stride, const uint32_t* valid_bits, int zero_invalid_queries,
+                    float scale, cudaStream_t stream) {
+  if (s.head_dim == 128)
+    return launch_fwd_t<128>(q, k, v, o, lse, s, q_stride, k_stride, v_stride, o_stride,
+                             valid_bits, zero_invalid_queries, scale, stream);
+  if (s.head_dim == 64)
+    return launch_fwd_t<64>(q, k, v, o, lse, s, q_stride, k_stride, v_stride, o_stride,
+                            valid_bits, zero_invalid_queries, scale, stream);
+  set_error("attention kernels support head_dim 64 or 128");
+  return kUnsupported;
+}
+
+}  // namespace osp

@@ -1,0 +1,67 @@
+// Internal (non-ABI) declarations shared by the .cu translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace osp {
+
+// Thread-local error message backing osp_last_error().
+void set_error(const std::string& msg);
+
+// Status codes (mirror include/osp_skiparse.h).
+enum Status : int {
+  kOk = 0,
+  kPattern = 1,
+  kShape = 2,
+  kCoordinate = 3,
+  kSharding = 4,
+  kCollective = 5,
+  kProtocol = 6,
+  kValue = 7,
+  kUnsupported = 8,
+  kCuda = 9,
+};
+
+int check_cuda(cudaError_t e, const char* what);
+
+// Build a 3-D bf16 TMA descriptor over a (n_seq, rows, cols) row-strided matrix with a
+// (64 x box_rows x 1) box and 128-byte swizzle.
+int make_tmap_bf16_3d(CUtensorMap* map, const void* base, int64_t cols, int64_t rows,
+                      int64_t n_seq, int64_t row_stride_elems, int box_rows);
+
+// Closed-form row map of the rearrange engine (rearrange.cu).
+struct MapParams {
+  int kind;
+  int64_t B;              // batch items (for SSP: local batch G*b)
+  int64_t T, H, W, k;     // padded grid (for SSP: the global padded grid)
+  int64_t H0, W0;         // original extents (== H, W when no padding)
+  int64_t G, bsub;        // SSP: subsequences per rank, batch items per subsequence group
+  const int64_t* table;   // kTable
+  int64_t n_in_rows;      // kTable bound
+};
+
+struct AttnShape {
+  int64_t n_seq, seq_len, heads, head_dim;
+};
+
+int launch_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                    const AttnShape& s, int64_t q_stride, int64_t k_stride, int64_t v_stride,
+                    int64_t o_stride, const uint32_t* valid_bits, int zero_invalid_queries,
+                    float scale, cudaStream_t stream);
+
+int launch_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                    const float* lse, void* dq, void* dk, void* dv, const AttnShape& s,
+                    int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t o_stride,
+                    int64_t do_stride, int64_t dq_stride, int64_t dk_stride, int64_t dv_stride,
+                    const uint32_t* valid_bits, int zero_invalid_queries, float scale,
+                    void* workspace, size_t workspace_bytes, cudaStream_t stream);
+size_t attn_bwd_workspace_bytes(const AttnShape& s);
+
+int launch_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,
+                     int d, cudaStream_t stream);
+
+}  // namespace osp

@@ -1,0 +1,213 @@
+"""Torch-tensor wrappers over the C ABI (one function per exported kernel).
+
+Tensors must be CUDA tensors; shapes/strides are checked here, semantics in the
+kernels.  These are the only functions that call into libosp_skiparse.so.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from .errors import ShapeError, UnsupportedError
+
+MAP_IDS = {"identity": 0, "orig_to_tsa": 1, "tsa_to_orig": 2, "orig_to_gsa": 3, "gsa_to_orig": 4,
+           "tsa_to_gsa": 5, "gsa_to_tsa": 6, "pad": 7, "strip": 8}
+PATTERN_IDS = {"original": 0, "tsa": 1, "gsa": 2}
+
+
+def _cuda(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the B200 path has no CPU fallback)")
+    return t
+
+
+def rearrange(x: torch.Tensor, map_name: str, t: int, h: int, w: int, k: int, batch: int,
+              h_orig: int | None = None, w_orig: int | None = None,
+              out: torch.Tensor | None = None) -> torch.Tensor:
+    """Apply one closed-form map to a (rows, seq, chan)-shaped tensor.  (t,h,w,k)
+    is the padded grid; output shape follows the map."""
+    L = _lib.lib()
+    _cuda(x, "x")
+    x = x.contiguous()
+    h0 = h if h_orig is None else h_orig
+    w0 = w if w_orig is None else w_orig
+    chan = x.shape[-1]
+    S, S0 = t * h * w, t * h0 * w0
+    n_sub = k * k
+    if map_name in ("orig_to_tsa", "orig_to_gsa"):
+        in_shape, out_shape = (batch, S0), (n_sub * batch, S // n_sub)
+    elif map_name in ("tsa_to_orig", "gsa_to_orig"):
+        in_shape, out_shape = (n_sub * batch, S // n_sub), (batch, S0)
+    elif map_name in ("tsa_to_gsa", "gsa_to_tsa"):
+        in_shape = out_shape = (n_sub * batch, S // n_sub)
+    elif map_name == "pad":
+        in_shape, out_shape = (batch, S0), (batch, S)
+    elif map_name == "strip":
+        in_shape, out_shape = (batch, S), (batch, S0)
+    elif map_name == "identity":
+        in_shape = out_shape = (batch, S)
+    else:
+        raise ValueError(f"unknown map {map_name!r}")
+    if x.numel() != in_shape[0] * in_shape[1] * chan:
+        raise ShapeError(f"map expects input ({in_shape[0]}, {in_shape[1]}, {chan}), got "
+                         f"{tuple(x.shape)}")
+    if out is None:
+        out = torch.empty((out_shape[0], out_shape[1], chan), dtype=x.dtype, device=x.device)
+    _lib.check(L.osp_rearrange(x.data_ptr(), out.data_ptr(), x.element_size(), chan, batch, t, h,
+                               w, k, MAP_IDS[map_name], h0, w0, _lib.stream_ptr(x.device)))
+    return out
+
+
+def gather_rows(x: torch.Tensor, index: torch.Tensor, n_out_rows: int) -> torch.Tensor:
+    """dst row i = src row index[i] (rows = leading (batch, seq) addresses)."""
+    L = _lib.lib()
+    _cuda(x, "x")
+    x = x.contiguous()
+    index = index.to(device=x.device, dtype=torch.int64).contiguous()
+    chan = x.shape[-1]
+    n_in = x.numel() // max(chan, 1) if chan else 0
+    out = torch.empty((n_out_rows, chan), dtype=x.dtype, device=x.device)
+    _lib.check(L.osp_gather_rows(x.data_ptr(), out.data_ptr(), index.data_ptr(), n_out_rows, n_in,
+                                 chan * x.element_size(), _lib.stream_ptr(x.device)))
+    return out
+
+
+def invert_index(index: torch.Tensor) -> torch.Tensor:
+    L = _lib.lib()
+    _cuda(index, "index")
+    index = index.contiguous().to(torch.int64)
+    inv = torch.full_like(index, -1)
+    _lib.check(L.osp_invert_index(index.data_ptr(), inv.data_ptr(), index.numel(),
+                                  _lib.stream_ptr(index.device)))
+    return inv
+
+
+def pattern_mask_bits(batch: int, t: int, h: int, w: int, k: int, pattern: str, h_orig: int,
+                      w_orig: int, device) -> torch.Tensor:
+    """(rows, ceil(L/32)) int32 bit words of the 1-D validity mask."""
+    L = _lib.lib()
+    n_sub = 1 if pattern == "original" else k * k
+    Ls = t * h * w // n_sub
+    bits = torch.empty((n_sub * batch, (Ls + 31) // 32), dtype=torch.int32, device=device)
+    _lib.check(L.osp_pattern_mask_bits(bits.data_ptr(), batch, t, h, w, k, PATTERN_IDS[pattern],
+                                       h_orig, w_orig, _lib.stream_ptr(device)))
+    return bits
+
+
+def bytes_to_bits(valid: torch.Tensor) -> torch.Tensor:
+    L = _lib.lib()
+    _cuda(valid, "valid")
+    v = valid.to(torch.uint8).contiguous()
+    rows, n = v.shape
+    bits = torch.empty((rows, (n + 31) // 32), dtype=torch.int32, device=v.device)
+    _lib.check(L.osp_mask_bytes_to_bits(v.data_ptr(), bits.data_ptr(), rows, n,
+                                        _lib.stream_ptr(v.device)))
+    return bits
+
+
+def bits_to_bytes(bits: torch.Tensor, n: int) -> torch.Tensor:
+    L = _lib.lib()
+    rows = bits.shape[0]
+    out = torch.empty((rows, n), dtype=torch.uint8, device=bits.device)
+    _lib.check(L.osp_mask_bits_to_bytes(bits.data_ptr(), out.data_ptr(), rows, n,
+                                        _lib.stream_ptr(bits.device)))
+    return out.bool()
+
+
+def _head_dim_plan(d: int) -> int:
+    if d in (64, 128):
+        return d
+    if 0 < d < 64:
+        return 64
+    if 64 < d < 128:
+        return 128
+    raise UnsupportedError(f"head_dim {d} > 128 is not supported by the B200 attention kernels")
+
+
+def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, heads: int, head_dim: int,
+             valid_bits: torch.Tensor | None, zero_invalid_queries: bool, scale: float,
+             out: torch.Tensor | None = None):
+    """q, k, v: (n_seq, L, >= heads*head_dim) bf16 views with unit column stride.
+    Returns (o (n_seq, L, heads*head_dim) bf16, lse (n_seq, heads, L) fp32)."""
+    L = _lib.lib()
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        _cuda(t, name)
+        if t.dtype != torch.bfloat16:
+            raise UnsupportedError(f"{name} must be bfloat16, got {t.dtype}")
+        if t.stride(-1) != 1 or t.stride(0) != t.shape[1] * t.stride(1):
+            raise ShapeError(f"{name} needs unit column stride and dense rows")
+    n_seq, seq_len = q.shape[0], q.shape[1]
+    if out is None:
+        out = torch.empty((n_seq, seq_len, heads * head_dim), dtype=torch.bfloat16, device=q.device)
+    lse = torch.empty((n_seq, heads, seq_len), dtype=torch.float32, device=q.device)
+    _lib.check(L.osp_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                              lse.data_ptr(), n_seq, seq_len, heads, head_dim, q.stride(1),
+                              k.stride(1), v.stride(1), out.stride(1), _lib.ptr(valid_bits),
+                              int(zero_invalid_queries), float(scale), _lib.stream_ptr(q.device)))
+    return out, lse
+
+
+def attn_bwd(q, k, v, o, do, lse, heads: int, head_dim: int, valid_bits, zero_invalid_queries: bool,
+             scale: float, dq=None, dk=None, dv=None):
+    L = _lib.lib()
+    n_seq, seq_len = q.shape[0], q.shape[1]
+    C = heads * head_dim
+    dev = q.device
+    do = do.contiguous() if do.stride(-1) != 1 else do
+    if dq is None:
+        dq = torch.empty((n_seq, seq_len, C), dtype=torch.bfloat16, device=dev)
+    if dk is None:
+        dk = torch.empty((n_seq, seq_len, C), dtype=torch.bfloat16, device=dev)
+    if dv is None:
+        dv = torch.empty((n_seq, seq_len, C), dtype=torch.bfloat16, device=dev)
+    ws_bytes = L.osp_attn_bwd_workspace_bytes(n_seq, seq_len, heads, head_dim)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    _lib.check(L.osp_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
+                              lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), n_seq,
+                              seq_len, heads, head_dim, q.stride(1), k.stride(1), v.stride(1),
+                              o.stride(1), do.stride(1), dq.stride(1), dk.stride(1), dv.stride(1),
+                              _lib.ptr(valid_bits), int(zero_invalid_queries), float(scale),
+                              ws.data_ptr(), ws_bytes, _lib.stream_ptr(dev)))
+    return dq, dk, dv
+
+
+def ssp_pack(x: torch.Tensor, group_size: int, t: int, h: int, w: int, k: int) -> torch.Tensor:
+    L = _lib.lib()
+    _cuda(x, "x")
+    x = x.contiguous()
+    local_batch, seq, chan = x.shape
+    out = torch.empty((k * k * local_batch, seq // (k * k), chan), dtype=x.dtype, device=x.device)
+    _lib.check(L.osp_ssp_pack(x.data_ptr(), out.data_ptr(), x.element_size(), chan, group_size,
+                              local_batch, t, h, w, k, _lib.stream_ptr(x.device)))
+    return out
+
+
+def ssp_unpack(recv: torch.Tensor, group_size: int, local_batch: int, t: int, h: int, w: int,
+               k: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    L = _lib.lib()
+    _cuda(recv, "recv")
+    recv = recv.contiguous()
+    chan = recv.shape[-1]
+    seq = t * h * w // (k * k)
+    if out is None:
+        out = torch.empty((local_batch, seq, chan), dtype=recv.dtype, device=recv.device)
+    _lib.check(L.osp_ssp_unpack(recv.data_ptr(), out.data_ptr(), recv.element_size(), chan,
+                                group_size, local_batch, t, h, w, k, _lib.stream_ptr(recv.device)))
+    return out
+
+
+def debug_mma(a: torch.Tensor, b: torch.Tensor, v: torch.Tensor):
+    L = _lib.lib()
+    d = a.shape[1]
+    s = torch.empty((128, 128), dtype=torch.float32, device=a.device)
+    o = torch.empty((128, d), dtype=torch.float32, device=a.device)
+    _lib.check(L.osp_debug_mma(a.data_ptr(), b.data_ptr(), v.data_ptr(), s.data_ptr(), o.data_ptr(),
+                               d, _lib.stream_ptr(a.device)))
+    return s, o
+
+
+def softmax_scale(d: int) -> float:
+    return 1.0 / math.sqrt(d)

@@ -1,0 +1,205 @@
+"""GPU parity of the C-ABI kernels against the CPU oracle and reference goldens.
+
+Bit-exact for index work (rearrange, SSP pack/unpack, masks); attention within
+the bf16 budget err(kernel) <= 2 * err(plain bf16 attention) + 1e-3 (max abs,
+both against the float64 oracle on identical bf16-rounded inputs)."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import osp_oracle as O
+from oracle.torch_ref import attention_ref
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev():
+    return torch.device("cuda")
+
+
+def test_debug_mma_forms(lib):
+    from paper_2605_28691_b200 import kernels
+    torch.manual_seed(0)
+    for d in (64, 128):
+        a = torch.randn(128, d, device=_dev()).bfloat16()
+        b = torch.randn(128, d, device=_dev()).bfloat16()
+        v = torch.randn(128, d, device=_dev()).bfloat16()
+        s, o = kernels.debug_mma(a, b, v)
+        s_ref = a.double() @ b.double().T
+        assert torch.allclose(s.double(), s_ref, atol=1e-2, rtol=1e-3), \
+            f"SS MMA d={d}: max err {(s.double() - s_ref).abs().max().item()}"
+        o_ref = s.bfloat16().double() @ v.double()
+        assert torch.allclose(o.double(), o_ref, atol=5e-2, rtol=1e-3), \
+            f"TS MMA d={d}: max err {(o.double() - o_ref).abs().max().item()}"
+
+
+def test_rearrange_matches_reference_tables(lib, golden, golden_meta):
+    from paper_2605_28691_b200 import kernels
+    maps = golden("maps")
+    n = 0
+    for m in golden_meta["maps"]:
+        if "key" not in m:
+            continue
+        t, h, w, k = m["grid"]
+        ib, is_ = m["in"]
+        # int64 iota through the kernel reproduces the table bit-exactly
+        iota = torch.arange(ib * is_, dtype=torch.int64, device=_dev()).view(ib, is_, 1)
+        out = kernels.rearrange(iota, m["map"], t, h, w, k, m["batch"])
+        assert np.array_equal(out.view(m["out"]).cpu().numpy(), maps[m["key"]]), m["key"]
+        n += 1
+    assert n > 100
+
+
+@pytest.mark.parametrize("dtype,chan", [(torch.float64, 3), (torch.bfloat16, 5120),
+                                        (torch.uint8, 7), (torch.float32, 130)])
+def test_rearrange_payload_bitexact(lib, dtype, chan):
+    from paper_2605_28691_b200 import kernels
+    g = O.Grid(3, 8, 12, 2)
+    for name in ("orig_to_tsa", "tsa_to_orig", "orig_to_gsa", "gsa_to_orig", "tsa_to_gsa",
+                 "gsa_to_tsa"):
+        B = 2
+        tab = O.map_table(name, g, B)
+        n_in = tab.size
+        x = (torch.randn(n_in, chan) * 100).to(dtype) if dtype != torch.uint8 else \
+            torch.randint(0, 255, (n_in, chan), dtype=torch.uint8)
+        ref = x[torch.from_numpy(tab.reshape(-1))].view(tab.shape[0], tab.shape[1], chan)
+        in_rows = (B, g.seq_len) if name.startswith("orig") else (4 * B, g.seq_len // 4)
+        out = kernels.rearrange(x.view(*in_rows, chan).to(_dev()), name, g.t, g.h, g.w, g.k, B)
+        assert torch.equal(out.cpu(), ref), name
+
+
+def test_fused_pad_and_strip(lib):
+    from paper_2605_28691_b200 import kernels
+    for grid in [(1, 5, 6, 2), (2, 45, 80, 2), (1, 13, 9, 4), (2, 30, 52, 2)]:
+        g = O.Grid(*grid)
+        pgr = O.padded_grid(g)
+        B, C = 2, 16
+        x = np.random.default_rng(0).standard_normal((B, g.seq_len, C))
+        xp = O.pad(x, g)
+        xt = torch.from_numpy(x).to(_dev())
+        # pad alone
+        got = kernels.rearrange(xt, "pad", pgr.t, pgr.h, pgr.w, pgr.k, B, g.h, g.w)
+        assert np.array_equal(got.cpu().numpy(), xp)
+        got = kernels.rearrange(torch.from_numpy(xp).to(_dev()), "strip", pgr.t, pgr.h, pgr.w, pgr.k,
+                                B, g.h, g.w)
+        assert np.array_equal(got.cpu().numpy(), x)
+        for pat in ("tsa", "gsa"):
+            fwd = O.map_table(O.PATTERN_FWD[pat], pgr, B)
+            want = O.apply_table(fwd, xp)
+            got = kernels.rearrange(xt, O.PATTERN_FWD[pat], pgr.t, pgr.h, pgr.w, pgr.k, B, g.h, g.w)
+            assert np.array_equal(got.cpu().numpy(), want), (grid, pat)
+            back = kernels.rearrange(got, O.PATTERN_INV[pat], pgr.t, pgr.h, pgr.w, pgr.k, B, g.h, g.w)
+            assert np.array_equal(back.cpu().numpy(), x), (grid, pat)
+
+
+def test_pattern_masks(lib, golden, golden_meta):
+    from paper_2605_28691_b200 import kernels
+    pad = golden("pad")
+    for m in golden_meta["pad"]:
+        g = O.Grid(*m["grid"])
+        p = O.padded_grid(g)
+        bits = kernels.pattern_mask_bits(1, p.t, p.h, p.w, p.k, "original", g.h, g.w, _dev())
+        assert np.array_equal(kernels.bits_to_bytes(bits, p.seq_len).view(-1).cpu().numpy(),
+                              pad[f"mask_{m['key']}"])
+        for pat in ("tsa", "gsa"):
+            key = f"submask_{pat}_{m['key']}"
+            if key not in pad.files:
+                continue
+            L = p.seq_len // (g.k * g.k)
+            bits = kernels.pattern_mask_bits(1, p.t, p.h, p.w, p.k, pat, g.h, g.w, _dev())
+            assert np.array_equal(kernels.bits_to_bytes(bits, L).cpu().numpy(), pad[key]), key
+
+
+def test_ssp_pack_unpack_matches_reference(lib, golden, golden_meta):
+    from paper_2605_28691_b200 import kernels
+    s = golden("ssp")
+    for m in golden_meta["ssp"]:
+        key = m["case"]
+        t, h, w, k = m["grid"]
+        n = m["n"]
+        shards = O.shard(s[f"{key}_in"], n)
+        send = [kernels.ssp_pack(torch.from_numpy(x).to(_dev()), n, t, h, w, k) for x in shards]
+        per = send[0].shape[0] // n
+        recv = [torch.cat([send[j][r * per:(r + 1) * per] for j in range(n)]) for r in range(n)]
+        out = [kernels.ssp_unpack(r_, n, shards[0].shape[0], t, h, w, k) for r_ in recv]
+        assert np.array_equal(torch.stack(out).cpu().numpy(), s[f"{key}_out"]), key
+
+
+def _bf16(x):
+    return torch.from_numpy(O.bf16_round(x)).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("n,L,heads,d,masked", [
+    (1, 128, 1, 64, False), (2, 256, 2, 128, False), (1, 300, 1, 128, False),
+    (3, 1000, 2, 64, True), (2, 2048, 1, 128, True), (1, 4160, 1, 128, False),
+    (4, 520, 3, 128, True)])
+def test_attention_forward_vs_oracle(lib, n, L, heads, d, masked):
+    from paper_2605_28691_b200 import kernels
+    rng = np.random.default_rng(L + heads)
+    C = heads * d
+    q, k, v = (_bf16(rng.standard_normal((n, L, C))) for _ in range(3))
+    valid = torch.from_numpy(rng.random((n, L)) > 0.25) if masked else None
+    bits = kernels.bytes_to_bits(valid.to(_dev())) if masked else None
+    o, lse = kernels.attn_fwd(q.to(_dev()), k.to(_dev()), v.to(_dev()), heads, d, bits, masked,
+                              1 / math.sqrt(d))
+    ref = attention_ref(q, k, v, heads, valid, masked)
+    pt = attention_ref(q, k, v, heads, valid, masked, upcast=False).double()
+    err = (o.cpu().double() - ref).abs().max().item()
+    err_pt = (pt - ref).abs().max().item()
+    print(f"fwd n={n} L={L} h={heads} d={d} mask={masked}: max|err| {err:.3e} (bf16 torch {err_pt:.3e})")
+    assert err <= 2 * err_pt + 1e-3
+    # LSE
+    qh = q.double().view(n, L, heads, d).transpose(1, 2)
+    kh = k.double().view(n, L, heads, d).transpose(1, 2)
+    s = qh @ kh.transpose(-1, -2) / math.sqrt(d)
+    if masked:
+        s = s.masked_fill(~valid[:, None, None, :], float("-inf"))
+    lse_ref = torch.logsumexp(s, dim=-1)
+    if masked:
+        lse_ref = lse_ref.masked_fill(~valid[:, None, :], float("inf"))
+    fin = torch.isfinite(lse_ref)
+    assert torch.equal(torch.isfinite(lse.cpu()), fin)
+    assert (lse.cpu().double()[fin] - lse_ref[fin]).abs().max().item() < 2e-3
+
+
+def test_attention_all_keys_masked_row_is_zero(lib):
+    from paper_2605_28691_b200 import kernels
+    n, L, d = 2, 200, 64
+    q, k, v = (torch.randn(n, L, d, device=_dev()).bfloat16() for _ in range(3))
+    valid = torch.ones(n, L, dtype=torch.bool, device=_dev())
+    valid[1] = False
+    o, lse = kernels.attn_fwd(q, k, v, 1, d, kernels.bytes_to_bits(valid), False, 0.125)
+    assert (o[1] == 0).all() and torch.isinf(lse[1]).all()
+    assert not (o[0] == 0).all()
+
+
+@pytest.mark.parametrize("n,L,heads,d,masked", [
+    (1, 128, 1, 64, False), (2, 384, 2, 128, True), (1, 1000, 1, 128, False),
+    (2, 700, 2, 64, True), (1, 2100, 1, 128, True)])
+def test_attention_backward_vs_autograd(lib, n, L, heads, d, masked):
+    from paper_2605_28691_b200 import kernels
+    rng = np.random.default_rng(7 * L + heads)
+    C = heads * d
+    q, k, v, do = (_bf16(rng.standard_normal((n, L, C))) for _ in range(4))
+    valid = torch.from_numpy(rng.random((n, L)) > 0.25) if masked else None
+    bits = kernels.bytes_to_bits(valid.to(_dev())) if masked else None
+    qd, kd, vd = q.to(_dev()), k.to(_dev()), v.to(_dev())
+    o, lse = kernels.attn_fwd(qd, kd, vd, heads, d, bits, masked, 1 / math.sqrt(d))
+    dq, dk, dv = kernels.attn_bwd(qd, kd, vd, o, do.to(_dev()), lse, heads, d, bits, masked,
+                                  1 / math.sqrt(d))
+    leaves = [t.double().requires_grad_() for t in (q, k, v)]
+    ref = attention_ref(*leaves, heads, valid, masked)
+    ref.backward(do.double())
+    lp = [t.detach().clone().requires_grad_() for t in (q, k, v)]
+    pt = attention_ref(*lp, heads, valid, masked, upcast=False)
+    pt.backward(do)
+    for name, got, r, p in zip("qkv", (dq, dk, dv), leaves, lp):
+        e = (got.cpu().double() - r.grad).abs().max().item()
+        e_pt = (p.grad.double() - r.grad).abs().max().item()
+        rel = e / max(r.grad.abs().max().item(), 1e-12)
+        print(f"bwd d{name} n={n} L={L} h={heads} d={d}: max|err| {e:.3e} rel {rel:.3e} "
+              f"(bf16 torch {e_pt:.3e})")
+        assert e <= 2 * e_pt + 2e-3, name
