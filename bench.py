@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Skiparse-2D attention block fwd+bwd throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3] [--impl ours|reference]
+
+One step = one Skiparse-2D block (token-wise application, then group-wise
+application, each = fixed q/k/v projection + per-subsequence attention, with
+the pattern switch between them) forward AND backward over one synthetic latent
+per SSP group, inputs resident in HBM (all inputs > 126 MB L2, so no flush is
+needed).  N > 1: one process per GPU (torchrun), Sparse Sequence Parallel over
+NCCL; k^2 % N != 0 (k=2, N=8) runs SSP4 x DP2 (two latents).
+
+Prints ONE JSON line on rank 0 (see the contract in the task spec): value =
+real latent tokens / s of the whole job, e2e = the same through the public API
+with the step's input copied from pinned host memory and the loss read back,
+roofline for the dominant kernel (attention backward), cpu_baseline = the CPU
+oracle (a port of the reference's numpy path) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (T, H, W, k, heads, head_dim, description) -- BASELINE.json configs
+    "cfg1": (4, 16, 16, 2, 4, 64, "4x16x16 latent, 4 heads x 64, k=2 (reference CPU case)"),
+    "cfg2": (21, 30, 52, 2, 12, 128, "Wan-1.3B shape 12x128 on 480p latent 21x30x52, k=2"),
+    "cfg3": (21, 45, 80, 2, 40, 128, "Wan-14B shape 40x128 on 720p latent 21x45x80, k=2"),
+    "cfg5k2": (33, 45, 80, 2, 40, 128, "Wan-14B shape on 129-frame 720p latent 33x45x80, k=2"),
+    "cfg5k4": (33, 45, 80, 4, 40, 128, "Wan-14B shape on 129-frame 720p latent 33x45x80, k=4"),
+}
+METRIC = "Skiparse-2D attn block tokens/s fwd+bwd"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["bf16_tflops"], d["bf16_tflops_sustained"], d["hbm_gbs"], "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        pw = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "power_w_max": max(pw) if pw else None, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+
+def _cpu_slice(args):
+    L, d, seed = args
+    import numpy as np
+    from oracle import osp_oracle as O
+    rng = np.random.default_rng(seed)
+    q, k, v = (rng.standard_normal((1, L, d)) for _ in range(3))
+    t0 = time.perf_counter()
+    O.dense_attention(q, k, v)
+    return time.perf_counter() - t0
+
+
+def cpu_oracle_rate(cfg, workers: int, L_sample: int = 2048, reps: int = 1):
+    """Time the CPU oracle (a port of the reference's float64 numpy dense_attention,
+    attention.py:47-67, single-threaded einsum) on (subsequence, head) slices of
+    length L_sample, `workers` slices in parallel, and extrapolate by L^2 to the
+    full block (2 applications x k^2 x heads slices of the padded length; backward
+    = 2.5 x forward since the reference has none)."""
+    T, H, W, k, heads, d, _ = CONFIGS[cfg]
+    k2 = k * k
+    Hp, Wp = -(-H // k2) * k2, -(-W // k2) * k2
+    L = T * Hp * Wp // k2
+    Ls = min(L_sample, L)
+    t0 = time.perf_counter()
+    if workers > 1:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(workers) as pool:
+            per = pool.map(_cpu_slice, [(Ls, d, i) for i in range(workers * reps)])
+    else:
+        per = [_cpu_slice((Ls, d, i)) for i in range(reps)]
+    wall = time.perf_counter() - t0
+    slices_per_s = len(per) / wall
+    n_slices = 2 * k2 * heads  # per block (batch 1)
+    sec_block_fwd = n_slices * (L / Ls) ** 2 / slices_per_s
+    sec_block = 3.5 * sec_block_fwd
+    tokens = T * H * W
+    return {"value": tokens / sec_block, "unit": "tokens/s", "cores": workers,
+            "sample": (f"{len(per)} float64 dense_attention slices of L={Ls}, d={d} in {wall:.2f} s "
+                       f"on {workers} process(es); extrapolated by (L/{Ls})^2 to L={L}, x{n_slices} "
+                       f"slices/block, bwd=2.5x fwd (reference has no backward)"),
+            "wall_s": wall}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    cores = os.cpu_count() or 1
+    T, H, W, k, heads, d, desc = CONFIGS[args.config]
+    rates = []
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_oracle_rate(args.config, cores, 1024)
+    for _ in range(args.steps):
+        rates.append(cpu_oracle_rate(args.config, cores, args.cpu_sample))
+    val = statistics.median(r["value"] for r in rates)
+    tokens = T * H * W
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * tokens / val, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "description": desc, "grid": [T, H, W], "k": k,
+                       "heads": heads, "head_dim": d, "global_batch": 1},
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": rates[-1]["sample"]},
+            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+
+def run_ours(args, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2605_28691_b200 import GridShape, kernels
+    from paper_2605_28691_b200.block import SkiparseBlock
+    from paper_2605_28691_b200.ssp import CommLog
+
+    T, H, W, k, heads, d, desc = CONFIGS[args.config]
+    k2 = k * k
+    C = heads * d
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    group, dp, ssp_n = None, 1, world
+    if world > 1:
+        if k2 % world == 0:
+            ssp_n = world
+        elif world % k2 == 0:
+            ssp_n, dp = k2, world // k2
+            groups = [dist.new_group(list(range(i * ssp_n, (i + 1) * ssp_n))) for i in range(dp)]
+            group = groups[rank // ssp_n]
+        else:
+            raise SystemExit(f"cannot shard k^2={k2} subsequences over {world} GPUs")
+    log = CommLog()
+    g = GridShape(T, H, W, k)
+    blk = SkiparseBlock(g, heads, C, batch=1, group=group if world > 1 else None, log=log,
+                        device=dev)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = torch.randn((blk.local_rows, blk.L, C), generator=gen, device=dev).to(torch.bfloat16)
+    gy = torch.randn((blk.local_rows, blk.L, C), generator=gen, device=dev).to(torch.bfloat16)
+    x.requires_grad_(True)
+
+    def step(inp):
+        y = blk(inp)
+        y.backward(gy)
+        return y
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        x.grad = None
+        step(x)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- device-resident timed region
+    kernels.STATS.reset(timing=True)
+    log.events.clear()
+    stream = torch.cuda.current_stream()
+    gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[local_rank]) \
+        if "CUDA_VISIBLE_DEVICES" in os.environ else local_rank
+    with ClockSampler(gpu_index) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            x.grad = None
+            step(x)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    launches = kernels.STATS.launches
+    per_kernel = kernels.STATS.elapsed_ms()
+    kernels.STATS.reset(timing=False)
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    ms_step = ms / args.steps
+    tokens_step = dp * T * H * W
+    value = tokens_step / (ms_step / 1000.0)
+
+    # ---- end-to-end through the public API (pinned host input, loss read back)
+    host_x = torch.empty((blk.local_rows, blk.L, C), dtype=torch.bfloat16, pin_memory=True)
+    host_x.copy_(x.detach().cpu())
+    host_loss = torch.empty((args.steps,), dtype=torch.float32, pin_memory=True)
+    xdev = torch.empty_like(x.detach())
+    barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for i in range(args.steps):
+        xdev.copy_(host_x, non_blocking=True)
+        xin = xdev.detach().requires_grad_(True)
+        y = blk(xin)
+        loss = (y.float() * gy.float()).sum()
+        y.backward(gy)
+        host_loss[i:i + 1].copy_(loss.detach().view(1), non_blocking=True)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t = torch.tensor([f0.elapsed_time(f1)], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms_step = t.item() / args.steps
+    e2e_value = tokens_step / (e2e_ms_step / 1000.0)
+
+    if rank != 0:
+        return
+    burst, sustained, hbm, peak_src = _peaks()
+    fl = blk.flops()
+    n_sub_local = blk.local_rows
+    att_fwd_launch = 4 * n_sub_local * blk.L * blk.L * d * heads
+    kern = {}
+    for name, v in per_kernel.items():
+        kern[name] = {"launches": len(v), "mean_ms": statistics.mean(v), "total_ms": sum(v)}
+    bwd = kern.get("attn_bwd")
+    fwd = kern.get("attn_fwd")
+    ach_bwd = 2.5 * att_fwd_launch / (bwd["mean_ms"] / 1e3) / 1e12 if bwd else None
+    ach_fwd = att_fwd_launch / (fwd["mean_ms"] / 1e3) / 1e12 if fwd else None
+    total_tflops = world * fl["total"] / (ms_step / 1e3) / 1e12 / world  # per GPU
+    roof = {"bound": "tensor", "kernel": "osp_attn_bwd (K3: delta prep + tcgen05 main + dq finalize)",
+            "achieved": ach_bwd, "peak": sustained, "unit": "TFLOP/s",
+            "frac": ach_bwd / sustained if ach_bwd else None,
+            "traffic": None, "peak_source": f"{peak_src} bf16 sustained (MEASURED_PEAKS.json)",
+            "algorithmic_flops_per_launch": 2.5 * att_fwd_launch,
+            "fwd_kernel": {"kernel": "osp_attn_fwd (K2)", "achieved": ach_fwd,
+                           "frac": ach_fwd / sustained if ach_fwd else None,
+                           "algorithmic_flops_per_launch": att_fwd_launch},
+            "block_tensor_tflops_per_gpu": total_tflops,
+            "block_frac_of_peak": total_tflops / sustained,
+            "block_frac_of_burst_peak": total_tflops / burst}
+    share = {n: v["total_ms"] / ms for n, v in kern.items()}
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong" if dp == 1 else "mixed",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn, bf16)",
+            "config": {"workload": args.config, "description": desc, "grid": [T, H, W], "k": k,
+                       "heads": heads, "head_dim": d, "global_batch": dp,
+                       "parallelism": (f"ssp{ssp_n}" + (f"xdp{dp}" if dp > 1 else "")),
+                       "padded_grid": [blk.grid.t, blk.grid.h, blk.grid.w], "subseq_len": blk.L,
+                       "l2": "inputs > 126 MB L2 (no flush needed)",
+                       "block": "TSA app + switch + GSA app + switch, each app = fixed QKV "
+                                "projection (cuBLAS) + tcgen05 attention; bwd = input grad"},
+            "e2e": {"value": e2e_value, "unit": "tokens/s",
+                    "h2d_bytes_per_step": host_x.numel() * host_x.element_size(),
+                    "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms_step},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "flops_per_step_per_gpu": fl,
+            "kernel_ms": kern, "kernel_share_of_step": share,
+            "comm": {"all_to_all_per_step": log.count("all_to_all") // max(args.steps, 1),
+                     "bytes_per_rank_per_step": log.total_bytes() // max(args.steps, 1),
+                     "ulysses_model_bytes_per_rank_per_step":
+                         4 * log.total_bytes() // max(args.steps, 1)} if world > 1 else None,
+            "clocks": clk.summary()}
+    if world == 1 and not args.no_cpu:
+        cb = cpu_oracle_rate(args.config, 1, args.cpu_sample, reps=2)
+        line["cpu_baseline"] = {k_: cb[k_] for k_ in ("value", "unit", "cores", "sample")}
+        line["cpu_baseline"]["kind"] = "port"
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=2048)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, world, rank, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

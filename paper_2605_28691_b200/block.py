@@ -1,0 +1,106 @@
+"""One Skiparse-2D attention block (token-wise application, then group-wise
+application) in the steady-state layout of a Skiparse DiT, single GPU or SSP.
+
+The reference operator is skiparse_attention (attention.py:97-131) applied
+with TOKEN_WISE and then GROUP_WISE; in a model the hidden states stay in a
+pattern layout between blocks, so the block maps a
+token-wise input to a token-wise output:
+
+    qkv1 = x W1 ; o1 = attn_tsa(qkv1)          (per subsequence, 1-D mask)
+    x2   = switch(o1)                           tsa_to_gsa (N=1) | SSP all-to-all
+    qkv2 = x2 W2 ; o2 = attn_gsa(qkv2)
+    y    = switch(o2)                           gsa_to_tsa (N=1) | SSP all-to-all
+
+Under SSP each rank holds G = k^2/N whole subsequences (ssp.py:91-106) and the
+switch is one NCCL all-to-all (ssp.py:139-180); attention needs no
+communication.  W1, W2 are the reference's fixed seeded projections
+(attention.py:20-32) in bf16; they are constants, so the backward produces the
+input gradient only.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import kernels
+from .anyres import PaddedGrid, pad_grid
+from .attention import COMPUTE_DTYPE, PROJECTION_SEED, attention_packed, packed_projection
+from .gridseq import GridShape, IndexMap
+from .skiparse import SparsePattern
+from .ssp import CommLog, ssp_switch
+
+
+class SkiparseBlock:
+    def __init__(self, g: GridShape, heads: int, chan: int, batch: int = 1, group=None,
+                 log: CommLog | None = None, device=None, seeds=(PROJECTION_SEED, PROJECTION_SEED + 1)):
+        import torch.distributed as dist
+        self.g = g
+        self.pg: PaddedGrid = pad_grid(g)
+        self.grid = self.pg.padded
+        self.heads, self.chan, self.batch = heads, chan, batch
+        self.group = group
+        self.world = dist.get_world_size(group) if (group is not None or (
+            dist.is_available() and dist.is_initialized())) else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        self.log = log
+        n_sub = g.k * g.k
+        if (n_sub * batch) % self.world:
+            raise ValueError(f"{n_sub * batch} subsequences do not shard over {self.world} ranks")
+        self.local_rows = n_sub * batch // self.world
+        self.L = self.grid.seq_len // n_sub
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.W1 = packed_projection(chan, COMPUTE_DTYPE, dev, seeds[0])
+        self.W2 = packed_projection(chan, COMPUTE_DTYPE, dev, seeds[1])
+        r0, r1 = self.rank * self.local_rows, (self.rank + 1) * self.local_rows
+        bt = self.pg.mask_bits(SparsePattern.TOKEN_WISE, batch)
+        bg = self.pg.mask_bits(SparsePattern.GROUP_WISE, batch)
+        self.bits_tsa = None if bt is None else bt[r0:r1].contiguous()
+        self.bits_gsa = None if bg is None else bg[r0:r1].contiguous()
+        self._t2g = IndexMap._pattern("tsa_to_gsa", self.grid, batch)
+        self._g2t = IndexMap._pattern("gsa_to_tsa", self.grid, batch)
+
+    # ------------------------------------------------------------------ pieces
+    def switch_to_gsa(self, x):
+        if self.world == 1:
+            return self._t2g.apply(x)
+        return ssp_switch(x, self.grid, self.group, self.log)
+
+    def switch_to_tsa(self, x):
+        if self.world == 1:
+            return self._g2t.apply(x)
+        return ssp_switch(x, self.grid, self.group, self.log)
+
+    def attend(self, x, W, bits):
+        qkv = torch.matmul(x, W)
+        return attention_packed(qkv, self.heads, bits, zero_invalid_queries=bits is not None)
+
+    def __call__(self, x_tsa: torch.Tensor) -> torch.Tensor:
+        """x_tsa: this rank's (G*B, L, C) bf16 shard in the token-wise layout."""
+        o1 = self.attend(x_tsa, self.W1, self.bits_tsa)
+        x2 = self.switch_to_gsa(o1)
+        o2 = self.attend(x2, self.W2, self.bits_gsa)
+        return self.switch_to_tsa(o2)
+
+    # ------------------------------------------------------------------ layouts
+    def to_local_tsa(self, x_orig: torch.Tensor) -> torch.Tensor:
+        """(B, T*H0*W0, C) unpadded original layout -> this rank's token-wise shard
+        (fused pad + orig_to_tsa, K1)."""
+        p = self.grid
+        full = kernels.rearrange(x_orig, "orig_to_tsa", p.t, p.h, p.w, p.k, self.batch,
+                                 self.g.h, self.g.w)
+        r0 = self.rank * self.local_rows
+        return full[r0:r0 + self.local_rows]
+
+    def flops(self) -> dict:
+        """Algorithmic tensor FLOPs of one block fwd+bwd for this rank, counted on
+        the padded grid as the reference's flop_report is (checks.py:144-146)."""
+        d = self.chan // self.heads
+        att_fwd = 4 * self.local_rows * self.L * self.L * d * self.heads  # per application
+        rows = self.local_rows * self.L
+        proj_fwd = 2 * rows * self.chan * 3 * self.chan  # x @ [Wq|Wk|Wv]
+        return {
+            "attention_fwd_per_app": att_fwd,
+            "attention_fwd_bwd": 2 * 3.5 * att_fwd,
+            "projection_fwd_bwd": 2 * 2 * proj_fwd,  # fwd GEMM + input-gradient GEMM
+            "total": 2 * 3.5 * att_fwd + 4 * proj_fwd,
+        }

@@ -18,6 +18,40 @@ MAP_IDS = {"identity": 0, "orig_to_tsa": 1, "tsa_to_orig": 2, "orig_to_gsa": 3, 
 PATTERN_IDS = {"original": 0, "tsa": 1, "gsa": 2}
 
 
+class LaunchStats:
+    """Counts this library's kernel launches and optionally brackets each C-ABI
+    call with CUDA events on the launching stream (bench.py uses both)."""
+
+    def __init__(self):
+        self.launches = 0
+        self.timing = False
+        self.events: dict = {}
+
+    def reset(self, timing: bool = False):
+        self.launches = 0
+        self.timing = timing
+        self.events = {}
+
+    def run(self, name: str, n_kernels: int, fn):
+        if self.timing:
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            rc = fn()
+            e.record()
+            self.events.setdefault(name, []).append((s, e))
+        else:
+            rc = fn()
+        self.launches += n_kernels
+        return rc
+
+    def elapsed_ms(self) -> dict:
+        return {k: [s.elapsed_time(e) for s, e in v] for k, v in self.events.items()}
+
+
+STATS = LaunchStats()
+
+
 def _cuda(t: torch.Tensor, name: str) -> torch.Tensor:
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (the B200 path has no CPU fallback)")
@@ -56,8 +90,8 @@ def rearrange(x: torch.Tensor, map_name: str, t: int, h: int, w: int, k: int, ba
                          f"{tuple(x.shape)}")
     if out is None:
         out = torch.empty((out_shape[0], out_shape[1], chan), dtype=x.dtype, device=x.device)
-    _lib.check(L.osp_rearrange(x.data_ptr(), out.data_ptr(), x.element_size(), chan, batch, t, h,
-                               w, k, MAP_IDS[map_name], h0, w0, _lib.stream_ptr(x.device)))
+    _lib.check(STATS.run('rearrange', 1, lambda: L.osp_rearrange(x.data_ptr(), out.data_ptr(), x.element_size(), chan, batch, t, h,
+                               w, k, MAP_IDS[map_name], h0, w0, _lib.stream_ptr(x.device))))
     return out
 
 
@@ -70,8 +104,8 @@ def gather_rows(x: torch.Tensor, index: torch.Tensor, n_out_rows: int) -> torch.
     chan = x.shape[-1]
     n_in = x.numel() // max(chan, 1) if chan else 0
     out = torch.empty((n_out_rows, chan), dtype=x.dtype, device=x.device)
-    _lib.check(L.osp_gather_rows(x.data_ptr(), out.data_ptr(), index.data_ptr(), n_out_rows, n_in,
-                                 chan * x.element_size(), _lib.stream_ptr(x.device)))
+    _lib.check(STATS.run('gather_rows', 1, lambda: L.osp_gather_rows(x.data_ptr(), out.data_ptr(), index.data_ptr(), n_out_rows, n_in,
+                                 chan * x.element_size(), _lib.stream_ptr(x.device))))
     return out
 
 
@@ -80,8 +114,8 @@ def invert_index(index: torch.Tensor) -> torch.Tensor:
     _cuda(index, "index")
     index = index.contiguous().to(torch.int64)
     inv = torch.full_like(index, -1)
-    _lib.check(L.osp_invert_index(index.data_ptr(), inv.data_ptr(), index.numel(),
-                                  _lib.stream_ptr(index.device)))
+    _lib.check(STATS.run('invert_index', 1, lambda: L.osp_invert_index(index.data_ptr(), inv.data_ptr(), index.numel(),
+                                  _lib.stream_ptr(index.device))))
     return inv
 
 
@@ -92,8 +126,8 @@ def pattern_mask_bits(batch: int, t: int, h: int, w: int, k: int, pattern: str, 
     n_sub = 1 if pattern == "original" else k * k
     Ls = t * h * w // n_sub
     bits = torch.empty((n_sub * batch, (Ls + 31) // 32), dtype=torch.int32, device=device)
-    _lib.check(L.osp_pattern_mask_bits(bits.data_ptr(), batch, t, h, w, k, PATTERN_IDS[pattern],
-                                       h_orig, w_orig, _lib.stream_ptr(device)))
+    _lib.check(STATS.run('mask_bits', 1, lambda: L.osp_pattern_mask_bits(bits.data_ptr(), batch, t, h, w, k, PATTERN_IDS[pattern],
+                                       h_orig, w_orig, _lib.stream_ptr(device))))
     return bits
 
 
@@ -103,8 +137,8 @@ def bytes_to_bits(valid: torch.Tensor) -> torch.Tensor:
     v = valid.to(torch.uint8).contiguous()
     rows, n = v.shape
     bits = torch.empty((rows, (n + 31) // 32), dtype=torch.int32, device=v.device)
-    _lib.check(L.osp_mask_bytes_to_bits(v.data_ptr(), bits.data_ptr(), rows, n,
-                                        _lib.stream_ptr(v.device)))
+    _lib.check(STATS.run('mask_bits', 1, lambda: L.osp_mask_bytes_to_bits(v.data_ptr(), bits.data_ptr(), rows, n,
+                                        _lib.stream_ptr(v.device))))
     return bits
 
 
@@ -112,8 +146,8 @@ def bits_to_bytes(bits: torch.Tensor, n: int) -> torch.Tensor:
     L = _lib.lib()
     rows = bits.shape[0]
     out = torch.empty((rows, n), dtype=torch.uint8, device=bits.device)
-    _lib.check(L.osp_mask_bits_to_bytes(bits.data_ptr(), out.data_ptr(), rows, n,
-                                        _lib.stream_ptr(bits.device)))
+    _lib.check(STATS.run('mask_bits', 1, lambda: L.osp_mask_bits_to_bytes(bits.data_ptr(), out.data_ptr(), rows, n,
+                                        _lib.stream_ptr(bits.device))))
     return out.bool()
 
 
@@ -143,10 +177,10 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, heads: int, head
     if out is None:
         out = torch.empty((n_seq, seq_len, heads * head_dim), dtype=torch.bfloat16, device=q.device)
     lse = torch.empty((n_seq, heads, seq_len), dtype=torch.float32, device=q.device)
-    _lib.check(L.osp_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+    _lib.check(STATS.run('attn_fwd', 1, lambda: L.osp_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                               lse.data_ptr(), n_seq, seq_len, heads, head_dim, q.stride(1),
                               k.stride(1), v.stride(1), out.stride(1), _lib.ptr(valid_bits),
-                              int(zero_invalid_queries), float(scale), _lib.stream_ptr(q.device)))
+                              int(zero_invalid_queries), float(scale), _lib.stream_ptr(q.device))))
     return out, lse
 
 
@@ -156,7 +190,8 @@ def attn_bwd(q, k, v, o, do, lse, heads: int, head_dim: int, valid_bits, zero_in
     n_seq, seq_len = q.shape[0], q.shape[1]
     C = heads * head_dim
     dev = q.device
-    do = do.contiguous() if do.stride(-1) != 1 else do
+    if do.stride(-1) != 1 or do.stride(0) != do.shape[1] * do.stride(1):
+        do = do.contiguous()
     if dq is None:
         dq = torch.empty((n_seq, seq_len, C), dtype=torch.bfloat16, device=dev)
     if dk is None:
@@ -165,12 +200,12 @@ def attn_bwd(q, k, v, o, do, lse, heads: int, head_dim: int, valid_bits, zero_in
         dv = torch.empty((n_seq, seq_len, C), dtype=torch.bfloat16, device=dev)
     ws_bytes = L.osp_attn_bwd_workspace_bytes(n_seq, seq_len, heads, head_dim)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    _lib.check(L.osp_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
+    _lib.check(STATS.run('attn_bwd', 3, lambda: L.osp_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
                               lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), n_seq,
                               seq_len, heads, head_dim, q.stride(1), k.stride(1), v.stride(1),
                               o.stride(1), do.stride(1), dq.stride(1), dk.stride(1), dv.stride(1),
                               _lib.ptr(valid_bits), int(zero_invalid_queries), float(scale),
-                              ws.data_ptr(), ws_bytes, _lib.stream_ptr(dev)))
+                              ws.data_ptr(), ws_bytes, _lib.stream_ptr(dev))))
     return dq, dk, dv
 
 
@@ -180,8 +215,8 @@ def ssp_pack(x: torch.Tensor, group_size: int, t: int, h: int, w: int, k: int) -
     x = x.contiguous()
     local_batch, seq, chan = x.shape
     out = torch.empty((k * k * local_batch, seq // (k * k), chan), dtype=x.dtype, device=x.device)
-    _lib.check(L.osp_ssp_pack(x.data_ptr(), out.data_ptr(), x.element_size(), chan, group_size,
-                              local_batch, t, h, w, k, _lib.stream_ptr(x.device)))
+    _lib.check(STATS.run('ssp_pack', 1, lambda: L.osp_ssp_pack(x.data_ptr(), out.data_ptr(), x.element_size(), chan, group_size,
+                              local_batch, t, h, w, k, _lib.stream_ptr(x.device))))
     return out
 
 
@@ -194,8 +229,8 @@ def ssp_unpack(recv: torch.Tensor, group_size: int, local_batch: int, t: int, h:
     seq = t * h * w // (k * k)
     if out is None:
         out = torch.empty((local_batch, seq, chan), dtype=recv.dtype, device=recv.device)
-    _lib.check(L.osp_ssp_unpack(recv.data_ptr(), out.data_ptr(), recv.element_size(), chan,
-                                group_size, local_batch, t, h, w, k, _lib.stream_ptr(recv.device)))
+    _lib.check(STATS.run('ssp_unpack', 1, lambda: L.osp_ssp_unpack(recv.data_ptr(), out.data_ptr(), recv.element_size(), chan,
+                                group_size, local_batch, t, h, w, k, _lib.stream_ptr(recv.device))))
     return out
 
 
