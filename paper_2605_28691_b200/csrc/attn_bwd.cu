@@ -18,6 +18,8 @@
 #include "osp_common.cuh"
 #include "osp_internal.h"
 
+#include <cstdlib>
+
 namespace osp {
 namespace {
 
@@ -48,6 +50,7 @@ struct BwdArgs {
   int words_per_seq;
   int seq_len, seq_pad, heads, n_q;
   float scale, scale_log2;
+  int flags;  // debug experiments (OSP_BWD_FLAGS): 1 = skip dQ atomics
 };
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tc_fence_before();
           mbar_arrive(bar_dqf);
         }
-        if (qg < a.seq_len) {
+        if (qg < a.seq_len && !(a.flags & 1)) {
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             red_add_v4(dst + cc * 32 + j * 4, __uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
@@ -367,6 +370,386 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// v2 main kernel for head_dim 128: 64-query tiles so TMEM holds a double-buffered dQ^T.
+//   TMEM: [0,64) S^T/P^T, [64,128) dP^T, [128,192) dQ^T buf0, [192,256) dQ^T buf1,
+//         [256,384) dV, [384,512) dK.
+//   dQ^T_i = K^T dS_i^T (M = d, N = 64 queries) is drained by four writer warps (thread = d)
+//   with 16-byte fp32 vector atomics into a (seq*head, q/4, d, q%4) accumulator, so a warp
+//   instruction covers 512 contiguous bytes; the MMA warp only waits for a buffer two
+//   iterations old, keeping the atomics off the tensor-core critical path.
+//   MMA order: S_0, dP_0, then per i: dV_i, S_{i+1}, dK_i, dQ^T_i, dP_{i+1}.
+struct BwdV2Layout {
+  static constexpr int kK = 0;                    // 128 keys x 128 d  (2 x 16 KB)
+  static constexpr int kV = 32768;
+  static constexpr int kStages = 3;
+  static constexpr int kQ = 65536;                // 3 x (64 q x 128 d = 2 x 8 KB)
+  static constexpr int kDO = kQ + kStages * 16384;
+  static constexpr int kDS = kDO + kStages * 16384;   // 2 x (128 keys x 64 q) bf16
+  static constexpr int kStat = kDS + 2 * 16384;       // 3 x (lse2[64], delta[64])
+  static constexpr int kBar = kStat + kStages * 512;
+  static constexpr int kSmem = kBar + 256;
+};
+
+__device__ __forceinline__ void red_add_v4_plain(float* addr, const uint32_t* v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_v2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                       const BwdArgs a) {
+  constexpr int D = 128;
+  using Ly = BwdV2Layout;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Ly::kBar);
+  uint64_t* bar_kv = bars + 0;
+  uint64_t* bar_qf = bars + 1;    // [3]
+  uint64_t* bar_qe = bars + 4;    // [3]
+  uint64_t* bar_s = bars + 7;
+  uint64_t* bar_dp = bars + 8;
+  uint64_t* bar_p = bars + 9;     // 128 arrivals
+  uint64_t* bar_ds = bars + 10;   // [2] 128 arrivals
+  uint64_t* bar_dsf = bars + 12;  // [2]
+  uint64_t* bar_dq = bars + 14;   // [2]
+  uint64_t* bar_dqf = bars + 16;  // [2] 128 arrivals
+  uint64_t* bar_fin = bars + 18;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int head = blockIdx.y;
+  const int seq = blockIdx.z;
+  const int kv0 = blockIdx.x * 128;
+  const int n_q = (a.seq_len + 63) / 64;
+
+  if ((smem_u32(sm) & 1023) != 0) __trap();
+  if (threadIdx.x == 0) {
+    mbar_init(bar_kv, 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(bar_qf + i, 1);
+      mbar_init(bar_qe + i, 1);
+    }
+    mbar_init(bar_s, 1);
+    mbar_init(bar_dp, 1);
+    mbar_init(bar_p, 128);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_ds + i, 128);
+      mbar_init(bar_dsf + i, 1);
+      mbar_init(bar_dq + i, 1);
+      mbar_init(bar_dqf + i, 128);
+    }
+    mbar_init(bar_fin, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tDP = tmem + 64, tDQ = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+  const int64_t sh = static_cast<int64_t>(seq) * a.heads + head;
+
+  if (warp < 4) {
+    regs_dec<120>();
+    if (warp == 0 && lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      tma_prefetch(&tmDO);
+      mbar_expect_tx(bar_kv, 65536);
+      for (int s = 0; s < 2; ++s) {
+        tma_load_3d(sm + Ly::kK + s * 16384, &tmK, bar_kv, head * D + s * 64, kv0, seq);
+        tma_load_3d(sm + Ly::kV + s * 16384, &tmV, bar_kv, head * D + s * 64, kv0, seq);
+      }
+      const float* lse2_g = a.lse2 + sh * a.seq_pad;
+      const float* delta_g = a.delta + sh * a.seq_pad;
+      for (int i = 0; i < n_q; ++i) {
+        const int st = i % 3;
+        mbar_wait(bar_qe + st, ((i / 3) & 1) ^ 1);
+        mbar_expect_tx(bar_qf + st, 2 * 16384 + 512);
+        for (int s = 0; s < 2; ++s) {
+          tma_load_3d(sm + Ly::kQ + st * 16384 + s * 8192, &tmQ, bar_qf + st, head * D + s * 64,
+                      i * 64, seq);
+          tma_load_3d(sm + Ly::kDO + st * 16384 + s * 8192, &tmDO, bar_qf + st, head * D + s * 64,
+                      i * 64, seq);
+        }
+        bulk_load(sm + Ly::kStat + st * 512, lse2_g + i * 64, 256, bar_qf + st);
+        bulk_load(sm + Ly::kStat + st * 512 + 256, delta_g + i * 64, 256, bar_qf + st);
+      }
+    } else if (warp == 1) {
+      // ---------------------------------------------------------------- MMA issuer (whole warp,
+      // one elected lane issues)
+      constexpr uint32_t kIdS = idesc_bf16(128, 64, 0, 0);     // S^T, dP^T
+      constexpr uint32_t kIdKV = idesc_bf16(128, 128, 0, 1);   // dV (TS), dK
+      constexpr uint32_t kIdQ = idesc_bf16(128, 64, 1, 1);     // dQ^T
+      const uint32_t tm = __shfl_sync(0xFFFFFFFFu, tmem, 0);
+      const uint32_t mS = tm, mDP = tm + 64, mDQ = tm + 128, mDV = tm + 256, mDK = tm + 384;
+      const uint32_t k_base = smem_u32(sm + Ly::kK);
+      const uint32_t v_base = smem_u32(sm + Ly::kV);
+      const uint32_t ds_base = smem_u32(sm + Ly::kDS);
+      const uint32_t q_base0 = smem_u32(sm + Ly::kQ);
+      const uint32_t do_base0 = smem_u32(sm + Ly::kDO);
+      auto issue_s = [&](int i) {
+        const uint32_t qb = q_base0 + (i % 3) * 16384;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ss(mS, sdesc_sw128(k_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                   sdesc_sw128(qb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), kIdS, kk > 0);
+          tc_commit(bar_s);
+        }
+        __syncwarp();
+      };
+      auto issue_dp = [&](int i) {
+        const uint32_t db = do_base0 + (i % 3) * 16384;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ss(mDP, sdesc_sw128(v_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                   sdesc_sw128(db + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), kIdS, kk > 0);
+          tc_commit(bar_dp);
+        }
+        __syncwarp();
+      };
+      mbar_wait(bar_kv, 0);
+      mbar_wait(bar_qf + 0, 0);
+      tc_fence_after();
+      issue_s(0);
+      issue_dp(0);
+      for (int i = 0; i < n_q; ++i) {
+        const int st = i % 3;
+        const int b = i & 1;
+        const uint32_t qb = q_base0 + st * 16384;
+        const uint32_t db = do_base0 + st * 16384;
+        // dV += P^T dO
+        mbar_wait(bar_p, i & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ts(mDV, mS + kk * 8, sdesc_sw128(db + kk * 2048, 8192, 1024), kIdKV,
+                   (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        __syncwarp();
+        // S_{i+1} (tS is free once dV_i has been issued: tcgen05 ops execute in order)
+        if (i + 1 < n_q) {
+          mbar_wait(bar_qf + (i + 1) % 3, ((i + 1) / 3) & 1);
+          tc_fence_after();
+          issue_s(i + 1);
+        }
+        // dK += dS^T Q
+        mbar_wait(bar_ds + b, (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t dsb = ds_base + b * 16384;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ss(mDK, sdesc_sw128(dsb + kk * 32, 16, 1024), sdesc_sw128(qb + kk * 2048, 8192, 1024),
+                   kIdKV, (i > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(bar_qe + st);
+        }
+        __syncwarp();
+        // dQ^T_i = K^T dS_i^T into buffer b (drained two iterations ago)
+        if (i >= 2) {
+          mbar_wait(bar_dqf + b, ((i - 2) >> 1) & 1);
+          tc_fence_after();
+        }
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ss(mDQ + b * 64, sdesc_sw128(k_base + kk * 2048, 16384, 1024),
+                   sdesc_sw128(dsb + kk * 2048, 8192, 1024), kIdQ, kk > 0);
+          tc_commit(bar_dq + b);
+          tc_commit(bar_dsf + b);
+        }
+        __syncwarp();
+        if (i + 1 < n_q) issue_dp(i + 1);
+      }
+      if (elect_one()) tc_commit(bar_fin);
+      __syncwarp();
+    }
+  } else if (warp < 8) {
+    regs_inc<232>();
+    // ------------------------------------------------------------------ compute warps (key rows)
+    const int wq = warp & 3;
+    const uint32_t la = static_cast<uint32_t>(wq * 32) << 16;
+    const int krow = wq * 32 + lane;
+    const int kglob = kv0 + krow;
+    bool kvalid = kglob < a.seq_len;
+    if (kvalid && a.valid_bits) {
+      const uint32_t* vb = a.valid_bits + static_cast<int64_t>(seq) * a.words_per_seq;
+      kvalid = (__ldg(vb + (kglob >> 5)) >> (kglob & 31)) & 1u;
+    }
+    const float c = a.scale_log2;
+    for (int i = 0; i < n_q; ++i) {
+      const int st = i % 3;
+      const int b = i & 1;
+      const float* lse_s = reinterpret_cast<const float*>(sm + Ly::kStat + st * 512);
+      const float* del_s = lse_s + 64;
+      mbar_wait(bar_qf + st, (i / 3) & 1);
+      mbar_wait(bar_s, i & 1);
+      tc_fence_after();
+      float p[64];
+      {
+        uint32_t s0[32], s1[32];
+        tmem_ld32(tS + la, s0);
+        tmem_ld32(tS + la + 32, s1);
+        tmem_wait_ld(s0);
+        tmem_wait_ld(s1);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 l0 = *reinterpret_cast<const float4*>(lse_s + j4 * 4);
+          const float4 l1 = *reinterpret_cast<const float4*>(lse_s + 32 + j4 * 4);
+          p[j4 * 4 + 0] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 0]), c, -l0.x));
+          p[j4 * 4 + 1] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 1]), c, -l0.y));
+          p[j4 * 4 + 2] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 2]), c, -l0.z));
+          p[j4 * 4 + 3] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 3]), c, -l0.w));
+          p[32 + j4 * 4 + 0] = ex2(fmaf(__uint_as_float(s1[j4 * 4 + 0]), c, -l1.x));
+          p[32 + j4 * 4 + 1] = ex2(fmaf(__uint_as_float(s1[j4 * 4 + 1]), c, -l1.y));
+          p[32 + j4 * 4 + 2] = ex2(fmaf(__uint_as_float(s1[j4 * 4 + 2]), c, -l1.z));
+          p[32 + j4 * 4 + 3] = ex2(fmaf(__uint_as_float(s1[j4 * 4 + 3]), c, -l1.w));
+        }
+      }
+      if (!kvalid) {
+#pragma unroll
+        for (int j = 0; j < 64; ++j) p[j] = 0.f;
+      }
+      {
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pk[j] = pack_bf16(p[2 * j], p[2 * j + 1]);
+        tmem_st32(tS + la, pk);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar_p);
+
+      mbar_wait(bar_dp, i & 1);
+      tc_fence_after();
+      if (i >= 2) mbar_wait(bar_dsf + b, ((i - 2) >> 1) & 1);
+      uint8_t* row = sm + Ly::kDS + b * 16384 + krow * 128;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t dp[32];
+        tmem_ld32(tDP + la + half * 32, dp);
+        tmem_wait_ld(dp);
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int q = half * 32 + 2 * j;
+          const float ds0 = p[q] * (__uint_as_float(dp[2 * j]) - del_s[q]);
+          const float ds1 = p[q + 1] * (__uint_as_float(dp[2 * j + 1]) - del_s[q + 1]);
+          pk[j] = pack_bf16(ds0, ds1);
+        }
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          const int phys = (half * 4 + ch) ^ (krow & 7);
+          *reinterpret_cast<uint4*>(row + phys * 16) =
+              make_uint4(pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(bar_ds + b);
+    }
+    // ------------------------------------------------------------------ dK / dV epilogue
+    mbar_wait(bar_fin, 0);
+    tc_fence_after();
+    const bool row_ok = kglob < a.seq_len;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t base = (which == 0 ? tDV : tDK) + la;
+      const float mul = which == 0 ? 1.f : a.scale;
+      __nv_bfloat16* dst =
+          (which == 0 ? a.dv : a.dk) +
+          (static_cast<int64_t>(seq) * a.seq_len + kglob) * (which == 0 ? a.dv_stride : a.dk_stride) +
+          static_cast<int64_t>(head) * D;
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t o[32];
+        tmem_ld32(base + cc * 32, o);
+        tmem_wait_ld(o);
+        if (row_ok) {
+          uint4 pk[4];
+          uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            pw[j] = pack_bf16(__uint_as_float(o[2 * j]) * mul, __uint_as_float(o[2 * j + 1]) * mul);
+          uint4* d4 = reinterpret_cast<uint4*>(dst + cc * 32);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) d4[j] = pk[j];
+        }
+      }
+    }
+  } else {
+    regs_dec<152>();
+    // ------------------------------------------------------------------ dQ^T writer warps (thread = d)
+    const int wq = warp & 3;
+    const uint32_t la = static_cast<uint32_t>(wq * 32) << 16;
+    const int dcol = wq * 32 + lane;
+    float* acc = a.dq_acc + sh * static_cast<int64_t>(a.seq_pad) * D;
+    for (int i = 0; i < n_q; ++i) {
+      const int b = i & 1;
+      mbar_wait(bar_dq + b, (i >> 1) & 1);
+      tc_fence_after();
+      uint32_t v0[32], v1[32];
+      tmem_ld32(tDQ + b * 64 + la, v0);
+      tmem_ld32(tDQ + b * 64 + la + 32, v1);
+      tmem_wait_ld(v0);
+      tmem_wait_ld(v1);
+      tc_fence_before();
+      mbar_arrive(bar_dqf + b);
+      if (!(a.flags & 1)) {
+        float* base = acc + (static_cast<int64_t>(i) * 16 * D + dcol) * 4;  // q/4 block = i*16
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) red_add_v4_plain(base + j4 * D * 4, v0 + j4 * 4);
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) red_add_v4_plain(base + (8 + j4) * D * 4, v1 + j4 * 4);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// dq = bf16(scale * acc) from the v2 (seq*head, q/4, d, q%4) accumulator.
+__global__ void dq_finalize_v2_kernel(const float* __restrict__ acc, __nv_bfloat16* dq, int64_t dq_stride,
+                                      int64_t n_seq, int heads, int seq_len, int seq_pad, float scale) {
+  constexpr int D = 128;
+  const int64_t nqb = seq_pad / 4;
+  const int64_t total = n_seq * heads * nqb * D;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int d = static_cast<int>(i % D);
+    int64_t r = i / D;
+    const int64_t qb = r % nqb;
+    const int64_t sh = r / nqb;
+    const int h = static_cast<int>(sh % heads);
+    const int64_t s = sh / heads;
+    const float4 v = reinterpret_cast<const float4*>(acc)[i];
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = qb * 4 + j;
+      if (q < seq_len)
+        dq[(s * seq_len + q) * dq_stride + static_cast<int64_t>(h) * D + d] = __float2bfloat16(vv[j] * scale);
+    }
   }
 }
 
@@ -430,7 +813,7 @@ BwdWs carve(void* ws, const AttnShape& s) {
   BwdWs w;
   uint8_t* p = static_cast<uint8_t*>(ws);
   w.dq_acc = reinterpret_cast<float*>(p);
-  p += ((s.n_seq * s.seq_len * s.heads * s.head_dim * 4 + 255) / 256) * 256;
+  p += ((s.n_seq * seq_pad * s.heads * s.head_dim * 4 + 255) / 256) * 256;
   w.lse2 = reinterpret_cast<float*>(p);
   p += ((s.n_seq * s.heads * seq_pad * 4 + 255) / 256) * 256;
   w.delta = reinterpret_cast<float*>(p);
@@ -451,7 +834,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
                  int64_t dvs, const uint32_t* bits, float scale, void* workspace, cudaStream_t stream) {
   const int64_t seq_pad = (s.seq_len + 127) / 128 * 128;
   BwdWs w = carve(workspace, s);
-  int rc = check_cuda(cudaMemsetAsync(w.dq_acc, 0, s.n_seq * s.seq_len * s.heads * D * 4, stream),
+  int rc = check_cuda(cudaMemsetAsync(w.dq_acc, 0, s.n_seq * seq_pad * s.heads * D * 4, stream),
                       "memset dq_acc");
   if (rc != kOk) return rc;
   {
@@ -465,10 +848,11 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
   }
   CUtensorMap mq, mk, mv, mdo;
   const int64_t cols = s.heads * D;
-  if ((rc = make_tmap_bf16_3d(&mq, q, cols, s.seq_len, s.n_seq, qs, 128)) != kOk) return rc;
+  const int qbox = D == 128 ? 64 : 128;
+  if ((rc = make_tmap_bf16_3d(&mq, q, cols, s.seq_len, s.n_seq, qs, qbox)) != kOk) return rc;
   if ((rc = make_tmap_bf16_3d(&mk, k, cols, s.seq_len, s.n_seq, ks, 128)) != kOk) return rc;
   if ((rc = make_tmap_bf16_3d(&mv, v, cols, s.seq_len, s.n_seq, vs, 128)) != kOk) return rc;
-  if ((rc = make_tmap_bf16_3d(&mdo, dout, cols, s.seq_len, s.n_seq, dos, 128)) != kOk) return rc;
+  if ((rc = make_tmap_bf16_3d(&mdo, dout, cols, s.seq_len, s.n_seq, dos, qbox)) != kOk) return rc;
   if ((dks * 2) % 16 || (dvs * 2) % 16 || (reinterpret_cast<uintptr_t>(dk) & 15) ||
       (reinterpret_cast<uintptr_t>(dv) & 15) || (dqs * 2) % 8 || (reinterpret_cast<uintptr_t>(dq) & 7)) {
     set_error("gradient outputs need 16-byte aligned bases/row strides");
@@ -490,16 +874,33 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
   a.n_q = static_cast<int>(seq_pad / 128);
   a.scale = scale;
   a.scale_log2 = scale * kLog2e;
+  {
+    const char* f = getenv("OSP_BWD_FLAGS");
+    a.flags = f ? atoi(f) : 0;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     rc = check_cuda(cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          BwdLayout<D>::kSmem),
                     "cudaFuncSetAttribute(attn_bwd)");
     if (rc != kOk) return rc;
+    rc = check_cuda(cudaFuncSetAttribute(attn_bwd_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         BwdV2Layout::kSmem),
+                    "cudaFuncSetAttribute(attn_bwd_v2)");
+    if (rc != kOk) return rc;
     attr_set = true;
   }
   dim3 grid(static_cast<unsigned>(seq_pad / 128), static_cast<unsigned>(s.heads),
             static_cast<unsigned>(s.n_seq));
+  if constexpr (D == 128) {
+    attn_bwd_v2_kernel<<<grid, kBwdThreads, BwdV2Layout::kSmem, stream>>>(mq, mk, mv, mdo, a);
+    rc = check_cuda(cudaGetLastError(), "attn_bwd_v2_kernel launch");
+    if (rc != kOk) return rc;
+    dq_finalize_v2_kernel<<<grid_for(s.n_seq * s.heads * seq_pad / 4 * D, 256), 256, 0, stream>>>(
+        w.dq_acc, static_cast<__nv_bfloat16*>(dq), dqs, s.n_seq, static_cast<int>(s.heads),
+        static_cast<int>(s.seq_len), static_cast<int>(seq_pad), scale);
+    return check_cuda(cudaGetLastError(), "dq_finalize_v2 launch");
+  }
   attn_bwd_kernel<D><<<grid, kBwdThreads, BwdLayout<D>::kSmem, stream>>>(mq, mk, mv, mdo, a);
   rc = check_cuda(cudaGetLastError(), "attn_bwd_kernel launch");
   if (rc != kOk) return rc;
@@ -513,7 +914,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
 
 size_t attn_bwd_workspace_bytes(const AttnShape& s) {
   const int64_t seq_pad = (s.seq_len + 127) / 128 * 128;
-  const int64_t a = ((s.n_seq * s.seq_len * s.heads * s.head_dim * 4 + 255) / 256) * 256;
+  const int64_t a = ((s.n_seq * seq_pad * s.heads * s.head_dim * 4 + 255) / 256) * 256;
   const int64_t b = ((s.n_seq * s.heads * seq_pad * 4 + 255) / 256) * 256;
   return static_cast<size_t>(a + 2 * b);
 }

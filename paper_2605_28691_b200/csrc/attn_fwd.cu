@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-    regs_dec<56>();
+    regs_dec<88>();
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
@@ -137,66 +137,69 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t kIdQK = idesc_bf16(kBM, kBN, 0, 0);
-      constexpr uint32_t kIdPV = idesc_bf16(kBM, D, 0, 1);
-      const uint32_t q_base = smem_u32(sm + Ly::kQ);
-      const uint32_t k_base = smem_u32(sm + Ly::kK);
-      const uint32_t v_base = smem_u32(sm + Ly::kV);
-      auto qk = [&](int t, int st) {
-        const uint32_t qa = q_base + t * Ly::kTile;
-        const uint32_t kb = k_base + st * Ly::kTile;
+    // ---------------------------------------------------------------- MMA issuer (whole warp
+    // runs the control flow; one elected lane issues, so operands stay warp-uniform)
+    constexpr uint32_t kIdQK = idesc_bf16(kBM, kBN, 0, 0);
+    constexpr uint32_t kIdPV = idesc_bf16(kBM, D, 0, 1);
+    const uint32_t tm = __shfl_sync(0xFFFFFFFFu, tmem, 0);
+    const uint32_t q_base = smem_u32(sm + Ly::kQ);
+    const uint32_t k_base = smem_u32(sm + Ly::kK);
+    const uint32_t v_base = smem_u32(sm + Ly::kV);
+    auto qk = [&](int t, int st, uint64_t* bar_a, uint64_t* bar_b) {
+      const uint32_t qa = q_base + t * Ly::kTile;
+      const uint32_t kb = k_base + st * Ly::kTile;
+      if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          mma_ss(tmem + t * 128, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
+          mma_ss(tm + t * 128, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
                  kIdQK, kk > 0);
         }
-      };
-      auto pv = [&](int t, int st, bool acc) {
-        const uint32_t vb = v_base + st * Ly::kTile;
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          mma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
-                 sdesc_sw128(vb + kk * 2048, 16384, 1024), kIdPV, (acc || kk > 0) ? 1u : 0u);
-        }
-      };
-      mbar_wait(bar_q + 0, 0);
-      mbar_wait(bar_q + 1, 0);
-      tc_fence_after();
-      for (int j = 0; j < a.n_kv; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(bar_kf + st, ph);
-        tc_fence_after();
-        qk(0, st);
-        tc_commit(bar_s + 0);
-        if (j > 0) {
-          mbar_wait(bar_p + 1, (j - 1) & 1);
-          tc_fence_after();
-          pv(1, (j - 1) & 1, j - 1 > 0);
-          tc_commit(bar_ve + ((j - 1) & 1));
-        }
-        qk(1, st);
-        tc_commit(bar_s + 1);
-        tc_commit(bar_ke + st);
-        mbar_wait(bar_vf + st, ph);
-        mbar_wait(bar_p + 0, j & 1);
-        tc_fence_after();
-        pv(0, st, j > 0);
+        tc_commit(bar_a);
+        if (bar_b) tc_commit(bar_b);
       }
-      const int last = a.n_kv - 1;
-      mbar_wait(bar_p + 1, last & 1);
+      __syncwarp();
+    };
+    auto pv = [&](int t, int st, bool acc, uint64_t* bar_a, uint64_t* bar_b, uint64_t* bar_c) {
+      const uint32_t vb = v_base + st * Ly::kTile;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          mma_ts(tm + 256 + t * 128, tm + t * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
+                 kIdPV, (acc || kk > 0) ? 1u : 0u);
+        if (bar_a) tc_commit(bar_a);
+        if (bar_b) tc_commit(bar_b);
+        if (bar_c) tc_commit(bar_c);
+      }
+      __syncwarp();
+    };
+    mbar_wait(bar_q + 0, 0);
+    mbar_wait(bar_q + 1, 0);
+    tc_fence_after();
+    for (int j = 0; j < a.n_kv; ++j) {
+      const int st = j & 1;
+      const uint32_t ph = (j >> 1) & 1;
+      mbar_wait(bar_kf + st, ph);
       tc_fence_after();
-      pv(1, last & 1, last > 0);
-      tc_commit(bar_ve + (last & 1));
-      tc_commit(bar_o + 0);
-      tc_commit(bar_o + 1);
+      qk(0, st, bar_s + 0, nullptr);
+      if (j > 0) {
+        mbar_wait(bar_p + 1, (j - 1) & 1);
+        tc_fence_after();
+        pv(1, (j - 1) & 1, j - 1 > 0, bar_ve + ((j - 1) & 1), nullptr, nullptr);
+      }
+      qk(1, st, bar_s + 1, bar_ke + st);
+      mbar_wait(bar_vf + st, ph);
+      mbar_wait(bar_p + 0, j & 1);
+      tc_fence_after();
+      pv(0, st, j > 0, nullptr, nullptr, nullptr);
     }
+    const int last = a.n_kv - 1;
+    mbar_wait(bar_p + 1, last & 1);
+    tc_fence_after();
+    pv(1, last & 1, last > 0, bar_ve + (last & 1), bar_o + 0, bar_o + 1);
   }
   } else {
-    regs_inc<224>();
+    regs_inc<208>();
     // -------------------------------------------------------------- softmax / epilogue
     const int t = (warp - 4) >> 2;
     const int wq = warp & 3;
