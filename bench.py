@@ -177,7 +177,7 @@ def run_ours(args, world, rank, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2605_28691_b200 import GridShape, kernels
-    from paper_2605_28691_b200.block import SkiparseBlock
+    from paper_2605_28691_b200.block import SkiparseBlock, plan_parallel
     from paper_2605_28691_b200.ssp import CommLog
 
     T, H, W, k, heads, d, desc = CONFIGS[args.config]
@@ -185,16 +185,11 @@ def run_ours(args, world, rank, local_rank):
     C = heads * d
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    group, dp, ssp_n = None, 1, world
-    if world > 1:
-        if k2 % world == 0:
-            ssp_n = world
-        elif world % k2 == 0:
-            ssp_n, dp = k2, world // k2
-            groups = [dist.new_group(list(range(i * ssp_n, (i + 1) * ssp_n))) for i in range(dp)]
-            group = groups[rank // ssp_n]
-        else:
-            raise SystemExit(f"cannot shard k^2={k2} subsequences over {world} GPUs")
+    group = None
+    ssp_n, dp = plan_parallel(world, k)
+    if dp > 1:
+        groups = [dist.new_group(list(range(i * ssp_n, (i + 1) * ssp_n))) for i in range(dp)]
+        group = groups[rank // ssp_n]
     log = CommLog()
     g = GridShape(T, H, W, k)
     blk = SkiparseBlock(g, heads, C, batch=1, group=group if world > 1 else None, log=log,

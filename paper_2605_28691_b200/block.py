@@ -30,6 +30,21 @@ from .skiparse import SparsePattern
 from .ssp import CommLog, ssp_switch
 
 
+def plan_parallel(world: int, k: int) -> tuple[int, int]:
+    """(SSP group size, data-parallel replicas) for `world` GPUs.  SSP shards the
+    k^2 subsequences of one latent over N ranks when N | k^2 (ssp.py:147-148);
+    otherwise (e.g. k=2 on 8 GPUs) groups of k^2 ranks run SSP and the groups
+    take different latents (SURVEY.md sec. 8e option 2)."""
+    k2 = k * k
+    if world < 1:
+        raise ValueError("world size must be positive")
+    if k2 % world == 0:
+        return world, 1
+    if world % k2 == 0:
+        return k2, world // k2
+    raise ValueError(f"cannot shard k^2={k2} subsequences over {world} ranks")
+
+
 class SkiparseBlock:
     def __init__(self, g: GridShape, heads: int, chan: int, batch: int = 1, group=None,
                  log: CommLog | None = None, device=None, seeds=(PROJECTION_SEED, PROJECTION_SEED + 1)):

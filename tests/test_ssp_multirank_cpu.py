@@ -1,0 +1,110 @@
+"""Multi-process SSP host logic on CPU: world_size 2 and 4 over gloo.
+
+The device pack/unpack kernels need a GPU, so here they are replaced (test-only
+monkeypatch) by the oracle's restatement of Alg. 1 steps 1 and 3-4; everything
+else is the product's distributed path (`ssp.ssp_switch` / `SSPSwitch`:
+guards, one all_to_all_single per switch, ledger, autograd backward)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import osp_oracle as O
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, grid, batch, pattern, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2605_28691_b200 import GridShape, kernels, ssp
+
+        og = O.Grid(*grid)
+
+        def pack(x, n, t, h, w, k):
+            return torch.from_numpy(O.ssp_pack(x.detach().numpy(), n, O.Grid(t, h, w, k)))
+
+        def unpack(recv, n, local_batch, t, h, w, k, out=None):
+            return torch.from_numpy(O.ssp_unpack(recv.numpy(), n, local_batch, O.Grid(t, h, w, k)))
+
+        kernels.ssp_pack = pack
+        kernels.ssp_unpack = unpack
+        rng = np.random.default_rng(11)
+        x_orig = rng.standard_normal((batch, og.seq_len, 3))
+        layout = O.apply_table(O.map_table(O.PATTERN_FWD[pattern], og, batch), x_orig)
+        shards = O.shard(layout, world)
+        want = O.ssp_switch(shards, og)[rank]
+        log = ssp.CommLog()
+        x = torch.from_numpy(shards[rank].copy()).requires_grad_(True)
+        y = ssp.ssp_switch(x, GridShape(*grid), None, log)
+        ok_fwd = np.array_equal(y.detach().numpy(), want)
+        gy = torch.from_numpy(rng.standard_normal(y.shape))
+        y.backward(gy)
+        # backward = the same self-inverse switch applied to the gradient
+        gshards = [None] * world
+        dist.all_gather_object(gshards, gy.numpy())
+        want_grad = O.ssp_switch(gshards, og)[rank]
+        ok_bwd = np.allclose(x.grad.numpy(), want_grad)
+        q.put((rank, ok_fwd, ok_bwd, log.count("all_to_all"), log.events[0].payload_per_rank,
+               shards[rank].size))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("grid,world,batch,pattern", [
+    ((1, 8, 8, 2), 2, 1, "tsa"), ((2, 8, 12, 2), 4, 1, "gsa"), ((1, 8, 8, 2), 2, 3, "gsa"),
+    ((1, 16, 16, 4), 4, 1, "tsa")])
+def test_ssp_switch_over_gloo(grid, world, batch, pattern):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, grid, batch, pattern, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert len(r) == 6, r
+        _, ok_fwd, ok_bwd, n_a2a, payload, local = r
+        assert ok_fwd and ok_bwd
+        assert n_a2a == 2  # one forward switch + one backward switch
+        assert payload == local  # ledger counts the whole per-rank buffer (ssp.py:135)
+
+
+def test_plan_parallel():
+    from paper_2605_28691_b200.block import plan_parallel
+    assert plan_parallel(1, 2) == (1, 1)
+    assert plan_parallel(2, 2) == (2, 1)
+    assert plan_parallel(4, 2) == (4, 1)
+    assert plan_parallel(8, 2) == (4, 2)   # SSP4 x DP2
+    assert plan_parallel(8, 4) == (8, 1)   # k=4: 16 subsequences over 8 ranks
+    with pytest.raises(ValueError):
+        plan_parallel(3, 2)
+
+
+def test_check_switch_guards():
+    from paper_2605_28691_b200 import GridShape, ProtocolError, ShardingError
+    from paper_2605_28691_b200.ssp import check_switch
+    g = GridShape(1, 8, 8, 2)
+    assert check_switch(2, 2, 16, g) == (2, 1)
+    with pytest.raises(ShardingError):
+        check_switch(3, 4, 16, g)
+    with pytest.raises(ProtocolError):
+        check_switch(2, 3, 16, g)
+    with pytest.raises(ProtocolError):
+        check_switch(2, 2, 15, g)
