@@ -151,9 +151,11 @@ def test_skiparse_attention_multihead_vs_oracle(P):
         got = P.skiparse_attention(torch.from_numpy(x).cuda(), g, P.SparsePattern(pat), pg,
                                    heads=2).cpu().numpy()
         want = O.skiparse_attention(x, og, pat, padded=padded, heads=2)
+        sim = O.skiparse_attention(x, og, pat, padded=padded, heads=2, round_fn=O.bf16_round)
         err = np.max(np.abs(got - want))
-        print(f"skiparse heads=2 {grid} {pat} padded={padded}: max|err| {err:.3e}")
-        assert err < 3e-2
+        budget = 2 * np.max(np.abs(sim - want)) + 1e-2
+        print(f"skiparse heads=2 {grid} {pat} padded={padded}: max|err| {err:.3e} budget {budget:.3e}")
+        assert err <= budget
 
 
 def test_pad_content_never_leaks(P):
