@@ -24,6 +24,7 @@ namespace osp {
 namespace {
 
 constexpr int kBwdThreads = 384;
+constexpr int kBwdV2Threads = 512;
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int D>
@@ -50,7 +51,7 @@ struct BwdArgs {
   int words_per_seq;
   int seq_len, seq_pad, heads, n_q;
   float scale, scale_log2;
-  int flags;  // debug experiments (OSP_BWD_FLAGS): 1 = skip dQ atomics
+  int flags;  // debug experiments (OSP_BWD_FLAGS): 1 = skip dQ atomics, 2 = skip compute math
 };
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -400,7 +401,7 @@ __device__ __forceinline__ void red_add_v4_plain(float* addr, const uint32_t* v)
                : "memory");
 }
 
-__global__ void __launch_bounds__(kBwdThreads, 1)
+__global__ void __launch_bounds__(kBwdV2Threads, 1)
     attn_bwd_v2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
                        const BwdArgs a) {
@@ -438,9 +439,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_init(bar_s, 1);
     mbar_init(bar_dp, 1);
-    mbar_init(bar_p, 128);
+    mbar_init(bar_p, 256);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(bar_ds + i, 128);
+      mbar_init(bar_ds + i, 256);
       mbar_init(bar_dsf + i, 1);
       mbar_init(bar_dq + i, 1);
       mbar_init(bar_dqf + i, 128);
@@ -460,8 +461,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int64_t sh = static_cast<int64_t>(seq) * a.heads + head;
 
   if (warp < 4) {
-    regs_dec<120>();
-    if (warp == 0 && lane == 0) {
+    if (warp == 0) {
+      if (elect_one()) {
       // ---------------------------------------------------------------- TMA producer
       tma_prefetch(&tmQ);
       tma_prefetch(&tmK);
@@ -487,9 +488,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         bulk_load(sm + Ly::kStat + st * 512, lse2_g + i * 64, 256, bar_qf + st);
         bulk_load(sm + Ly::kStat + st * 512 + 256, delta_g + i * 64, 256, bar_qf + st);
       }
+      }
+      __syncwarp();
     } else if (warp == 1) {
-      // ---------------------------------------------------------------- MMA issuer (whole warp,
-      // one elected lane issues)
+      // ---------------------------------------------------------------- MMA issuer (one elected lane runs
+      // the whole loop; operands are derived from warp-uniform values, so they live in
+      // uniform registers and no per-GEMM reconvergence is needed)
       constexpr uint32_t kIdS = idesc_bf16(128, 64, 0, 0);     // S^T, dP^T
       constexpr uint32_t kIdKV = idesc_bf16(128, 128, 0, 1);   // dV (TS), dK
       constexpr uint32_t kIdQ = idesc_bf16(128, 64, 1, 1);     // dQ^T
@@ -502,26 +506,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint32_t do_base0 = smem_u32(sm + Ly::kDO);
       auto issue_s = [&](int i) {
         const uint32_t qb = q_base0 + (i % 3) * 16384;
-        if (elect_one()) {
+        {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             mma_ss(mS, sdesc_sw128(k_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                    sdesc_sw128(qb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), kIdS, kk > 0);
           tc_commit(bar_s);
         }
-        __syncwarp();
       };
       auto issue_dp = [&](int i) {
         const uint32_t db = do_base0 + (i % 3) * 16384;
-        if (elect_one()) {
+        {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             mma_ss(mDP, sdesc_sw128(v_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                    sdesc_sw128(db + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), kIdS, kk > 0);
           tc_commit(bar_dp);
         }
-        __syncwarp();
       };
+      if (elect_one()) {
       mbar_wait(bar_kv, 0);
       mbar_wait(bar_qf + 0, 0);
       tc_fence_after();
@@ -535,13 +538,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // dV += P^T dO
         mbar_wait(bar_p, i & 1);
         tc_fence_after();
-        if (elect_one()) {
+        {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             mma_ts(mDV, mS + kk * 8, sdesc_sw128(db + kk * 2048, 8192, 1024), kIdKV,
                    (i > 0 || kk > 0) ? 1u : 0u);
         }
-        __syncwarp();
         // S_{i+1} (tS is free once dV_i has been issued: tcgen05 ops execute in order)
         if (i + 1 < n_q) {
           mbar_wait(bar_qf + (i + 1) % 3, ((i + 1) / 3) & 1);
@@ -552,20 +554,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(bar_ds + b, (i >> 1) & 1);
         tc_fence_after();
         const uint32_t dsb = ds_base + b * 16384;
-        if (elect_one()) {
+        {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             mma_ss(mDK, sdesc_sw128(dsb + kk * 32, 16, 1024), sdesc_sw128(qb + kk * 2048, 8192, 1024),
                    kIdKV, (i > 0 || kk > 0) ? 1u : 0u);
           tc_commit(bar_qe + st);
         }
-        __syncwarp();
         // dQ^T_i = K^T dS_i^T into buffer b (drained two iterations ago)
         if (i >= 2) {
           mbar_wait(bar_dqf + b, ((i - 2) >> 1) & 1);
           tc_fence_after();
         }
-        if (elect_one()) {
+        {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             mma_ss(mDQ + b * 64, sdesc_sw128(k_base + kk * 2048, 16384, 1024),
@@ -573,15 +574,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tc_commit(bar_dq + b);
           tc_commit(bar_dsf + b);
         }
-        __syncwarp();
         if (i + 1 < n_q) issue_dp(i + 1);
       }
-      if (elect_one()) tc_commit(bar_fin);
+      tc_commit(bar_fin);
+      }
       __syncwarp();
     }
-  } else if (warp < 8) {
-    regs_inc<232>();
-    // ------------------------------------------------------------------ compute warps (key rows)
+  } else if (warp < 12) {
+    // ------------------------------------------------------------------ compute warps: thread =
+    // key row, the two warpgroups split the 64 query columns of a tile (32 each)
+    const int half = (warp - 4) >> 2;
     const int wq = warp & 3;
     const uint32_t la = static_cast<uint32_t>(wq * 32) << 16;
     const int krow = wq * 32 + lane;
@@ -595,41 +597,44 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int i = 0; i < n_q; ++i) {
       const int st = i % 3;
       const int b = i & 1;
-      const float* lse_s = reinterpret_cast<const float*>(sm + Ly::kStat + st * 512);
+      const float* lse_s = reinterpret_cast<const float*>(sm + Ly::kStat + st * 512) + half * 32;
       const float* del_s = lse_s + 64;
       mbar_wait(bar_qf + st, (i / 3) & 1);
       mbar_wait(bar_s, i & 1);
       tc_fence_after();
-      float p[64];
+      if (a.flags & 2) {  // experiment: synchronisation skeleton only
+        tc_fence_before();
+        mbar_arrive(bar_p);
+        mbar_wait(bar_dp, i & 1);
+        if (i >= 2) mbar_wait(bar_dsf + b, ((i - 2) >> 1) & 1);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(bar_ds + b);
+        continue;
+      }
+      float p[32];
       {
-        uint32_t s0[32], s1[32];
-        tmem_ld32(tS + la, s0);
-        tmem_ld32(tS + la + 32, s1);
+        uint32_t s0[32];
+        tmem_ld32(tS + la + half * 32, s0);
         tmem_wait_ld(s0);
-        tmem_wait_ld(s1);
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
           const float4 l0 = *reinterpret_cast<const float4*>(lse_s + j4 * 4);
-          const float4 l1 = *reinterpret_cast<const float4*>(lse_s + 32 + j4 * 4);
           p[j4 * 4 + 0] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 0]), c, -l0.x));
           p[j4 * 4 + 1] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 1]), c, -l0.y));
           p[j4 * 4 + 2] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 2]), c, -l0.z));
           p[j4 * 4 + 3] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 3]), c, -l0.w));
-          p[32 + j4 * 4 + 0] = ex2(fmaf(__uint_as_float(s1[j4 * 4 + 0]), c, -l1.x));
-          p[32 + j4 * 4 + 1] = ex2(fmaf(__uint_as_float(s1[j4 * 4 + 1]), c, -l1.y));
-          p[32 + j4 * 4 + 2] = ex2(fmaf(__uint_as_float(s1[j4 * 4 + 2]), c, -l1.z));
-          p[32 + j4 * 4 + 3] = ex2(fmaf(__uint_as_float(s1[j4 * 4 + 3]), c, -l1.w));
         }
       }
       if (!kvalid) {
 #pragma unroll
-        for (int j = 0; j < 64; ++j) p[j] = 0.f;
+        for (int j = 0; j < 32; ++j) p[j] = 0.f;
       }
       {
-        uint32_t pk[32];
+        uint32_t pk[16];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) pk[j] = pack_bf16(p[2 * j], p[2 * j + 1]);
-        tmem_st32(tS + la, pk);
+        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(p[2 * j], p[2 * j + 1]);
+        tmem_st16(tS + la + half * 16, pk);
       }
       tmem_wait_st();
       tc_fence_before();
@@ -639,17 +644,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_after();
       if (i >= 2) mbar_wait(bar_dsf + b, ((i - 2) >> 1) & 1);
       uint8_t* row = sm + Ly::kDS + b * 16384 + krow * 128;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
+      {
         uint32_t dp[32];
         tmem_ld32(tDP + la + half * 32, dp);
         tmem_wait_ld(dp);
         uint32_t pk[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int q = half * 32 + 2 * j;
-          const float ds0 = p[q] * (__uint_as_float(dp[2 * j]) - del_s[q]);
-          const float ds1 = p[q + 1] * (__uint_as_float(dp[2 * j + 1]) - del_s[q + 1]);
+          const float2 d2 = *reinterpret_cast<const float2*>(del_s + 2 * j);
+          const float ds0 = p[2 * j] * (__uint_as_float(dp[2 * j]) - d2.x);
+          const float ds1 = p[2 * j + 1] * (__uint_as_float(dp[2 * j + 1]) - d2.y);
           pk[j] = pack_bf16(ds0, ds1);
         }
 #pragma unroll
@@ -664,11 +668,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_arrive(bar_ds + b);
     }
     // ------------------------------------------------------------------ dK / dV epilogue
+    // (warpgroup 0 drains dV, warpgroup 1 drains dK)
     mbar_wait(bar_fin, 0);
     tc_fence_after();
     const bool row_ok = kglob < a.seq_len;
-#pragma unroll
-    for (int which = 0; which < 2; ++which) {
+    {
+      const int which = half;
       const uint32_t base = (which == 0 ? tDV : tDK) + la;
       const float mul = which == 0 ? 1.f : a.scale;
       __nv_bfloat16* dst =
@@ -693,7 +698,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else {
-    regs_dec<152>();
     // ------------------------------------------------------------------ dQ^T writer warps (thread = d)
     const int wq = warp & 3;
     const uint32_t la = static_cast<uint32_t>(wq * 32) << 16;
@@ -893,7 +897,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
   dim3 grid(static_cast<unsigned>(seq_pad / 128), static_cast<unsigned>(s.heads),
             static_cast<unsigned>(s.n_seq));
   if constexpr (D == 128) {
-    attn_bwd_v2_kernel<<<grid, kBwdThreads, BwdV2Layout::kSmem, stream>>>(mq, mk, mv, mdo, a);
+    attn_bwd_v2_kernel<<<grid, kBwdV2Threads, BwdV2Layout::kSmem, stream>>>(mq, mk, mv, mdo, a);
     rc = check_cuda(cudaGetLastError(), "attn_bwd_v2_kernel launch");
     if (rc != kOk) return rc;
     dq_finalize_v2_kernel<<<grid_for(s.n_seq * s.heads * seq_pad / 4 * D, 256), 256, 0, stream>>>(

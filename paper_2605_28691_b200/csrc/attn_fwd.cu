@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp < 4) {
     regs_dec<88>();
   if (warp == 0) {
-    if (lane == 0) {
+    if (elect_one()) {
       // ------------------------------------------------------------ TMA producer
       tma_prefetch(&tmQ);
       tma_prefetch(&tmK);
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     auto qk = [&](int t, int st, uint64_t* bar_a, uint64_t* bar_b) {
       const uint32_t qa = q_base + t * Ly::kTile;
       const uint32_t kb = k_base + st * Ly::kTile;
-      if (elect_one()) {
+      {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
@@ -158,11 +158,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc_commit(bar_a);
         if (bar_b) tc_commit(bar_b);
       }
-      __syncwarp();
     };
     auto pv = [&](int t, int st, bool acc, uint64_t* bar_a, uint64_t* bar_b, uint64_t* bar_c) {
       const uint32_t vb = v_base + st * Ly::kTile;
-      if (elect_one()) {
+      {
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk)
           mma_ts(tm + 256 + t * 128, tm + t * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
@@ -171,8 +170,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (bar_b) tc_commit(bar_b);
         if (bar_c) tc_commit(bar_c);
       }
-      __syncwarp();
     };
+    if (elect_one()) {
     mbar_wait(bar_q + 0, 0);
     mbar_wait(bar_q + 1, 0);
     tc_fence_after();
@@ -197,6 +196,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     mbar_wait(bar_p + 1, last & 1);
     tc_fence_after();
     pv(1, last & 1, last > 0, bar_ve + (last & 1), bar_o + 0, bar_o + 1);
+    }
+    __syncwarp();
   }
   } else {
     regs_inc<208>();

@@ -61,6 +61,7 @@ int launch_attn_bwd(const void* q, const void* k, const void* v, const void* o, 
                     void* workspace, size_t workspace_bytes, cudaStream_t stream);
 size_t attn_bwd_workspace_bytes(const AttnShape& s);
 
+
 int launch_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,
                      int d, cudaStream_t stream);
 
