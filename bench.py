@@ -243,21 +243,39 @@ def run_ours(args, world, rank, local_rank):
     tokens_step = dp * T * H * W
     value = tokens_step / (ms_step / 1000.0)
 
-    # ---- end-to-end through the public API (pinned host input, loss read back)
+    # ---- end-to-end through the public API (pinned host input, loss read back).  Every step's
+    # input is copied host->device inside the timed region; the copy of step i+1 runs on a
+    # copy stream (double buffer) while step i computes, as a training loop's data feed would.
     host_x = torch.empty((blk.local_rows, blk.L, C), dtype=torch.bfloat16, pin_memory=True)
     host_x.copy_(x.detach().cpu())
     host_loss = torch.empty((args.steps,), dtype=torch.float32, pin_memory=True)
-    xdev = torch.empty_like(x.detach())
+    bufs = [torch.empty_like(x.detach()) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    copy_stream = torch.cuda.Stream(device=dev)
     barrier()
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
+    copy_stream.wait_stream(stream)
+    with torch.cuda.stream(copy_stream):
+        bufs[0].copy_(host_x, non_blocking=True)
+        ready[0].record(copy_stream)
     for i in range(args.steps):
-        xdev.copy_(host_x, non_blocking=True)
-        xin = xdev.detach().requires_grad_(True)
+        b = i % 2
+        if i + 1 < args.steps:
+            nb = (i + 1) % 2
+            with torch.cuda.stream(copy_stream):
+                if i >= 1:
+                    copy_stream.wait_event(consumed[nb])
+                bufs[nb].copy_(host_x, non_blocking=True)
+                ready[nb].record(copy_stream)
+        stream.wait_event(ready[b])
+        xin = bufs[b].detach().requires_grad_(True)
         y = blk(xin)
         loss = (y.float() * gy.float()).sum()
         y.backward(gy)
+        consumed[b].record(stream)
         host_loss[i:i + 1].copy_(loss.detach().view(1), non_blocking=True)
     f1.record(stream)
     torch.cuda.synchronize()

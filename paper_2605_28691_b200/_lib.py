@@ -12,7 +12,8 @@ from pathlib import Path
 
 from . import errors
 
-_PATH = Path(__file__).resolve().with_name("libosp_skiparse.so")
+_PATH = Path(os.environ["OSP_LIB"]) if os.environ.get("OSP_LIB") else \
+    Path(__file__).resolve().with_name("libosp_skiparse.so")
 _LIB = None
 
 c_i64 = ctypes.c_int64

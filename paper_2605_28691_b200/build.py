@@ -10,7 +10,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-LIB = PKG / "libosp_skiparse.so"
+LIB = Path(os.environ["OSP_LIB_OUT"]) if os.environ.get("OSP_LIB_OUT") else PKG / "libosp_skiparse.so"
 SOURCES = ["abi.cu", "rearrange.cu", "attn_fwd.cu", "attn_bwd.cu", "debug_mma.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -30,10 +30,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     jobs = []
     for s in SOURCES:
-        obj = CSRC / (s + ".o")
+        obj = LIB.parent / (LIB.name + "." + s + ".o")
         cmd = [NVCC, "-c", str(CSRC / s), "-o", str(obj), "-O3", "-std=c++17",
                "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-               "-Xcompiler", "-fPIC", "-I", str(ROOT / "include"), "--expt-relaxed-constexpr"]
+               "-Xcompiler", "-fPIC", "-I", str(ROOT / "include"), "--expt-relaxed-constexpr",
+               *os.environ.get("OSP_NVCC_FLAGS", "").split()]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         jobs.append((cmd, s))
