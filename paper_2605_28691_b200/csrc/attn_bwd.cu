@@ -51,6 +51,8 @@ struct BwdArgs {
   int words_per_seq;
   int seq_len, seq_pad, heads, n_q;
   float scale, scale_log2;
+  const __nv_bfloat16* k_rows;  // K (for the TMEM copy of the key tile)
+  int64_t k_row_stride;
   int flags;  // debug experiments (OSP_BWD_FLAGS): 1 = skip dQ atomics, 2 = skip compute math
 };
 
@@ -60,6 +62,30 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// Copy one 128-d bf16 row (global, 16B aligned) into 64 TMEM columns of this thread's lane in
+// the kind::f16 A-operand layout (column c = elements 2c, 2c+1); rows past the end -> 0.
+__device__ __forceinline__ void row_to_tmem(uint32_t taddr, const __nv_bfloat16* row, bool ok) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t r[32];
+    if (ok) {
+      const uint4* src = reinterpret_cast<const uint4*>(row + h * 64);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 v = __ldg(src + i);
+        r[4 * i + 0] = v.x;
+        r[4 * i + 1] = v.y;
+        r[4 * i + 2] = v.z;
+        r[4 * i + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = 0u;
+    }
+    tmem_st32(taddr + h * 32, r);
+  }
 }
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
@@ -421,6 +447,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
   uint64_t* bar_dq = bars + 14;   // [2]
   uint64_t* bar_dqf = bars + 16;  // [2] 128 arrivals
   uint64_t* bar_fin = bars + 18;
+  uint64_t* bar_kt = bars + 19;   // K rows in TMEM (256 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
   const int warp = threadIdx.x >> 5;
@@ -447,6 +474,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       mbar_init(bar_dqf + i, 128);
     }
     mbar_init(bar_fin, 1);
+    mbar_init(bar_kt, 256);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -457,7 +485,8 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tDP = tmem + 64, tDQ = tmem + 128, tDV = tmem + 256, tDK = tmem + 384;
+  const uint32_t tK = tmem, tS = tmem + 64, tDP = tmem + 128, tDQ = tmem + 192, tDV = tmem + 256,
+                 tDK = tmem + 384;
   const int64_t sh = static_cast<int64_t>(seq) * a.heads + head;
 
   if (warp < 4) {
@@ -498,7 +527,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       constexpr uint32_t kIdKV = idesc_bf16(128, 128, 0, 1);   // dV (TS), dK
       constexpr uint32_t kIdQ = idesc_bf16(128, 64, 1, 1);     // dQ^T
       const uint32_t tm = __shfl_sync(0xFFFFFFFFu, tmem, 0);
-      const uint32_t mS = tm, mDP = tm + 64, mDQ = tm + 128, mDV = tm + 256, mDK = tm + 384;
+      const uint32_t mK = tm, mS = tm + 64, mDP = tm + 128, mDQ = tm + 192, mDV = tm + 256, mDK = tm + 384;
       const uint32_t k_base = smem_u32(sm + Ly::kK);
       const uint32_t v_base = smem_u32(sm + Ly::kV);
       const uint32_t ds_base = smem_u32(sm + Ly::kDS);
@@ -509,8 +538,8 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            mma_ss(mS, sdesc_sw128(k_base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                   sdesc_sw128(qb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), kIdS, kk > 0);
+            mma_ts(mS, mK + kk * 8, sdesc_sw128(qb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024), kIdS,
+                   kk > 0);
           tc_commit(bar_s);
         }
       };
@@ -526,6 +555,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       };
       if (elect_one()) {
       mbar_wait(bar_kv, 0);
+      mbar_wait(bar_kt, 0);
       mbar_wait(bar_qf + 0, 0);
       tc_fence_after();
       issue_s(0);
@@ -555,23 +585,24 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         tc_fence_after();
         const uint32_t dsb = ds_base + b * 16384;
         {
+          // dK += dS^T Q with dS^T read from TMEM (TS; written over the consumed dP^T columns)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_ss(mDK, sdesc_sw128(dsb + kk * 32, 16, 1024), sdesc_sw128(qb + kk * 2048, 8192, 1024),
-                   kIdKV, (i > 0 || kk > 0) ? 1u : 0u);
+            mma_ts(mDK, mDP + kk * 8, sdesc_sw128(qb + kk * 2048, 8192, 1024), kIdKV,
+                   (i > 0 || kk > 0) ? 1u : 0u);
           tc_commit(bar_qe + st);
         }
-        // dQ^T_i = K^T dS_i^T into buffer b (drained two iterations ago)
-        if (i >= 2) {
-          mbar_wait(bar_dqf + b, ((i - 2) >> 1) & 1);
+        // dQ^T_i = K^T dS_i^T (single TMEM buffer; the writers drain it right after it lands)
+        if (i >= 1) {
+          mbar_wait(bar_dqf, (i - 1) & 1);
           tc_fence_after();
         }
         {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            mma_ss(mDQ + b * 64, sdesc_sw128(k_base + kk * 2048, 16384, 1024),
+            mma_ss(mDQ, sdesc_sw128(k_base + kk * 2048, 16384, 1024),
                    sdesc_sw128(dsb + kk * 2048, 8192, 1024), kIdQ, kk > 0);
-          tc_commit(bar_dq + b);
+          tc_commit(bar_dq);
           tc_commit(bar_dsf + b);
         }
         if (i + 1 < n_q) issue_dp(i + 1);
@@ -593,6 +624,12 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       const uint32_t* vb = a.valid_bits + static_cast<int64_t>(seq) * a.words_per_seq;
       kvalid = (__ldg(vb + (kglob >> 5)) >> (kglob & 31)) & 1u;
     }
+    if (half == 0)
+      row_to_tmem(tK + la, a.k_rows + (static_cast<int64_t>(seq) * a.seq_len + kglob) * a.k_row_stride +
+                               static_cast<int64_t>(head) * D, kglob < a.seq_len);
+    tmem_wait_st();
+    tc_fence_before();
+    mbar_arrive(bar_kt);
     const float c = a.scale_log2;
     for (int i = 0; i < n_q; ++i) {
       const int st = i % 3;
@@ -662,7 +699,11 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
           *reinterpret_cast<uint4*>(row + phys * 16) =
               make_uint4(pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
         }
+        // both warpgroups must have read dP^T before either overwrites it with dS^T
+        named_bar_sync(1, 256);
+        tmem_st16(tDP + la + half * 16, pk);
       }
+      tmem_wait_st();
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(bar_ds + b);
@@ -704,16 +745,15 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
     const int dcol = wq * 32 + lane;
     float* acc = a.dq_acc + sh * static_cast<int64_t>(a.seq_pad) * D;
     for (int i = 0; i < n_q; ++i) {
-      const int b = i & 1;
-      mbar_wait(bar_dq + b, (i >> 1) & 1);
+      mbar_wait(bar_dq, i & 1);
       tc_fence_after();
       uint32_t v0[32], v1[32];
-      tmem_ld32(tDQ + b * 64 + la, v0);
-      tmem_ld32(tDQ + b * 64 + la + 32, v1);
+      tmem_ld32(tDQ + la, v0);
+      tmem_ld32(tDQ + la + 32, v1);
       tmem_wait_ld(v0);
       tmem_wait_ld(v1);
       tc_fence_before();
-      mbar_arrive(bar_dqf + b);
+      mbar_arrive(bar_dqf);
       if (!(a.flags & 1)) {
         float* base = acc + (static_cast<int64_t>(i) * 16 * D + dcol) * 4;  // q/4 block = i*16
 #pragma unroll
@@ -878,6 +918,8 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
   a.n_q = static_cast<int>(seq_pad / 128);
   a.scale = scale;
   a.scale_log2 = scale * kLog2e;
+  a.k_rows = static_cast<const __nv_bfloat16*>(k);
+  a.k_row_stride = ks;
   {
     const char* f = getenv("OSP_BWD_FLAGS");
     a.flags = f ? atoi(f) : 0;
