@@ -401,13 +401,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------------------
-// v2 main kernel for head_dim 128: 64-query tiles so TMEM holds a double-buffered dQ^T.
-//   TMEM: [0,64) S^T/P^T, [64,128) dP^T, [128,192) dQ^T buf0, [192,256) dQ^T buf1,
-//         [256,384) dV, [384,512) dK.
-//   dQ^T_i = K^T dS_i^T (M = d, N = 64 queries) is drained by four writer warps (thread = d)
-//   with 16-byte fp32 vector atomics into a (seq*head, q/4, d, q%4) accumulator, so a warp
-//   instruction covers 512 contiguous bytes; the MMA warp only waits for a buffer two
-//   iterations old, keeping the atomics off the tensor-core critical path.
+// Main kernel for head_dim 128.  One CTA per (128-key tile, head, subsequence) streams 64-query
+// tiles.  Shared-memory operand bandwidth (128 B/clk/SM for tcgen05 SS mode, measured with
+// tools/mma_rate.cu) is the binding resource, so operands that can live in TMEM do:
+//   TMEM: [0,64) K (A operand of S^T, copied once), [64,128) S^T then P^T,
+//         [128,192) dP^T then dS^T, [192,256) dQ^T, [256,384) dV, [384,512) dK.
+//   S^T = K Q^T (TS), dP^T = V dO^T (SS), dV += P^T dO (TS), dK += dS^T Q (TS),
+//   dQ^T_i = K^T dS_i^T (SS, dS^T also staged in smem as the B operand).
+//   dQ^T is drained by four writer warps (thread = d) with 16-byte fp32 vector atomics into a
+//   (seq*head, q/4, d, q%4) accumulator so a warp instruction covers 512 contiguous bytes.
+//   Eight compute warps (thread = key row) split each tile's 64 query columns.
 //   MMA order: S_0, dP_0, then per i: dV_i, S_{i+1}, dK_i, dQ^T_i, dP_{i+1}.
 struct BwdV2Layout {
   static constexpr int kK = 0;                    // 128 keys x 128 d  (2 x 16 KB)
