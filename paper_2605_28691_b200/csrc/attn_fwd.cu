@@ -19,6 +19,8 @@
 #include "osp_common.cuh"
 #include "osp_internal.h"
 
+#include <cstdlib>
+
 namespace osp {
 namespace {
 
@@ -50,6 +52,7 @@ struct FwdArgs {
   int n_kv;
   float scale_log2;
   int zero_invalid_q;
+  int flags;  // debug experiments (OSP_FWD_FLAGS): 1 = no exp, 2 = softmax skeleton only
 };
 
 __device__ __forceinline__ bool bit_at(const uint32_t* bits, int words, int i) {
@@ -211,12 +214,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const uint32_t* vbits =
         a.valid_bits ? a.valid_bits + static_cast<int64_t>(seq) * a.words_per_seq : nullptr;
     const float c = a.scale_log2;
+    // The two softmax warpgroups share the SM's MUFU (16 ex2/clk).  Their exp phases are
+    // serialised in tile order (named barriers 2 and 3, ping-pong) so each tile's softmax
+    // finishes within the window the other tile's MMAs cover, instead of both running at half
+    // speed.  Warpgroup 1 opens the first turn for warpgroup 0.
+    const uint32_t my_turn = 2 + t, next_turn = 3 - t;
+    if (t == 1) asm volatile("bar.arrive %0, 256;" ::"r"(2u) : "memory");
 
     float m_used = -INFINITY;
     float l = 0.f;
     for (int j = 0; j < a.n_kv; ++j) {
       mbar_wait(bar_s + t, j & 1);
       tc_fence_after();
+      if (a.flags & 2) {
+        tc_fence_before();
+        mbar_arrive(bar_p + t);
+        continue;
+      }
       uint32_t s[4][32];
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) tmem_ld32(tS + cc * 32, s[cc]);
@@ -273,17 +287,24 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       const float ms = (m_used == -INFINITY) ? 0.f : m_used * c;
       float ls0 = 0.f, ls1 = 0.f;
+      named_bar_sync(my_turn, 256);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = ex2(fmaf(__uint_as_float(s[cc][2 * i]), c, -ms));
-          const float p1 = ex2(fmaf(__uint_as_float(s[cc][2 * i + 1]), c, -ms));
+          float p0 = fmaf(__uint_as_float(s[cc][2 * i]), c, -ms);
+          float p1 = fmaf(__uint_as_float(s[cc][2 * i + 1]), c, -ms);
+          if (!(a.flags & 1)) {
+            p0 = ex2(p0);
+            p1 = ex2(p1);
+          }
           ls0 += p0;
           ls1 += p1;
           pk[i] = pack_bf16(p0, p1);
         }
+        if (cc == 3 && !(t == 1 && j == a.n_kv - 1))
+          asm volatile("bar.arrive %0, 256;" ::"r"(next_turn) : "memory");
         tmem_st16(tS + cc * 16, pk);
       }
       tmem_wait_st();
@@ -354,6 +375,10 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
   a.n_kv = static_cast<int>((s.seq_len + kBN - 1) / kBN);
   a.scale_log2 = scale * 1.4426950408889634f;
   a.zero_invalid_q = zero_invalid_q;
+  {
+    const char* fl = getenv("OSP_FWD_FLAGS");
+    a.flags = fl ? atoi(fl) : 0;
+  }
   const int n_qt = static_cast<int>((s.seq_len + kBM - 1) / kBM);
   dim3 grid((n_qt + 1) / 2, static_cast<unsigned>(s.heads), static_cast<unsigned>(s.n_seq));
   static bool attr_set = false;

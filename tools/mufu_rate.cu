@@ -1,0 +1,54 @@
+// Microbenchmark: MUFU.EX2 vs polynomial exp2 (FMA pipe) throughput per SM.
+#include <cstdio>
+#include "../paper_2605_28691_b200/csrc/osp_common.cuh"
+using namespace osp;
+
+__device__ __forceinline__ float poly1(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;
+  const float j = t - 12582912.f;
+  const float f = x - j;
+  float p = fmaf(f, 0.05500893f, 0.24221099f);
+  p = fmaf(p, f, 0.69328293f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k(float* out, int iters, long long* cyc) {
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = -0.001f * (threadIdx.x + i);
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (MODE == 0) v[i] = ex2(v[i]) - 1.0f;
+      else v[i] = poly1(v[i]) - 1.0f;
+    }
+  }
+  long long t1 = clock64();
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += v[i];
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+
+template <int MODE>
+void run(int threads) {
+  float* o; long long* c;
+  cudaMalloc(&o, 4); cudaMalloc(&c, 8);
+  const int iters = 4000;
+  k<MODE><<<148, threads>>>(o, 10, c);
+  cudaDeviceSynchronize();
+  k<MODE><<<148, threads>>>(o, iters, c);
+  cudaDeviceSynchronize();
+  long long cyc; cudaMemcpy(&cyc, c, 8, cudaMemcpyDeviceToHost);
+  printf("%s threads=%d: %.1f exp2/clk/SM\n", MODE == 0 ? "MUFU.EX2" : "poly   ", threads,
+         double(threads) * iters * 16 / double(cyc));
+}
+int main() {
+  for (int t : {128, 256}) { run<0>(t); run<1>(t); }
+  return 0;
+}
