@@ -202,8 +202,18 @@ def ssp_golden():
     return arrays, meta, {"errors": errors, "comm": comm, "ulysses": uly, "naive": naive}
 
 
+def formats_golden():
+    """Byte-exact reference files: OSPT tensor (gridseq.py:232-256) and mask file
+    (anyres.py:99-112)."""
+    x = gridseq.random_tensor(2, 7, 3, seed=9)
+    gridseq.write_ospt(OUT / "ref_x.ospt", x)
+    pg = anyres.pad_grid(gridseq.GridShape(1, 5, 6, 2))
+    anyres.write_mask(OUT / "ref_mask_1x5x6_k2.bin", pg)
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
+    formats_golden()
     a_maps, m_maps = maps_golden()
     np.savez_compressed(OUT / "maps.npz", **a_maps)
     a_pad, m_pad = pad_golden()

@@ -1,0 +1,198 @@
+"""Hybrid Skiparse DiT attention stack: full-attention blocks at
+both ends, alternating token-wise / group-wise Skiparse blocks in the middle
+(`build_layer_schedule`, skiparse.py:221-237).
+
+Layout: the hidden states live in a pattern layout (token-wise or group-wise) for the whole
+stack.  Attention is permutation-equivariant (test_attention.py:140-149), so a FULL block runs
+directly on that layout: per batch item it attends over all k^2 subsequences concatenated,
+keyed by the concatenated subsequence masks.  No rearrange is needed at Full<->Skiparse
+boundaries; TSA<->GSA transitions are one `tsa_to_gsa` / `gsa_to_tsa` map (N=1) or one SSP
+all-to-all (N>1).
+
+Multi-GPU: Skiparse blocks use SSP (whole subsequences per rank, no communication inside
+attention).  FULL blocks use Ulysses head parallelism: one all-to-all turns
+the packed [q|k|v] of this rank's subsequences (all heads) into all subsequences for
+heads/N heads, and one all-to-all returns the output -- the Ulysses four-collective volume
+(ssp.py:183-191) in two calls.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import kernels
+from .anyres import pad_grid
+from .attention import COMPUTE_DTYPE, PROJECTION_SEED, attention_packed, packed_projection
+from .gridseq import GridShape, IndexMap
+from .skiparse import LayerKind, SparsePattern, build_layer_schedule
+from .ssp import CommLog, ssp_switch
+
+__all__ = ["HybridStack", "full_sequence_bits", "ulysses_qkv_to_heads", "ulysses_out_to_rows"]
+
+
+def full_sequence_bits(sub_bits: torch.Tensor, n_sub: int, batch: int, L: int) -> torch.Tensor:
+    """Key-validity bits of each batch item's full sequence in a pattern layout: the k^2
+    subsequence masks (rows nested (pattern id, batch item)) concatenated in pattern order."""
+    valid = kernels.bits_to_bytes(sub_bits, L).view(n_sub, batch, L)
+    full = valid.permute(1, 0, 2).reshape(batch, n_sub * L).contiguous()
+    return kernels.bytes_to_bits(full)
+
+
+def ulysses_qkv_to_heads(qkv_local: torch.Tensor, n: int, group=None, log: CommLog | None = None):
+    """(R, L, 3C) packed q|k|v of this rank's R pattern rows, all heads  ->  (N*R, L, 3C/N) of
+    all rows for this rank's C/N channels (heads), via one all_to_all_single."""
+    import torch.distributed as dist
+    R, L, C3 = qkv_local.shape
+    C = C3 // 3
+    send = qkv_local.view(R, L, 3, n, C // n).permute(3, 0, 1, 2, 4).contiguous()
+    recv = torch.empty_like(send)
+    dist.all_to_all_single(recv, send, group=group)
+    if log is not None:
+        log.record("all_to_all", send.numel(), "ulysses-qkv", send.numel() * send.element_size())
+    return recv.view(n * R, L, 3 * (C // n))
+
+
+def ulysses_out_to_rows(o_heads: torch.Tensor, n: int, group=None, log: CommLog | None = None):
+    """(N*R, L, C/N) output for this rank's heads -> (R, L, C) this rank's rows, all heads."""
+    import torch.distributed as dist
+    NR, L, Cn = o_heads.shape
+    R = NR // n
+    recv = torch.empty_like(o_heads)
+    dist.all_to_all_single(recv, o_heads.contiguous(), group=group)
+    if log is not None:
+        log.record("all_to_all", o_heads.numel(), "ulysses-out", o_heads.numel() * o_heads.element_size())
+    return recv.view(n, R, L, Cn).permute(1, 2, 0, 3).reshape(R, L, n * Cn)
+
+
+class _UlyssesQKV(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, qkv, n, group, log):
+        ctx.n, ctx.group, ctx.log = n, group, log
+        return ulysses_qkv_to_heads(qkv, n, group, log)
+
+    @staticmethod
+    def backward(ctx, g):
+        # adjoint of the row->head redistribution: send each head block back to its rows
+        import torch.distributed as dist
+        n = ctx.n
+        NR, L, C3n = g.shape
+        R = NR // n
+        recv = torch.empty_like(g)
+        dist.all_to_all_single(recv, g.contiguous(), group=ctx.group)
+        if ctx.log is not None:
+            ctx.log.record("all_to_all", g.numel(), "ulysses-qkv-bwd", g.numel() * g.element_size())
+        Cn = C3n // 3
+        out = recv.view(n, R, L, 3, Cn).permute(1, 2, 3, 0, 4).reshape(R, L, 3 * n * Cn)
+        return out, None, None, None
+
+
+class _UlyssesOut(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, o, n, group, log):
+        ctx.n, ctx.group, ctx.log = n, group, log
+        return ulysses_out_to_rows(o, n, group, log)
+
+    @staticmethod
+    def backward(ctx, g):
+        import torch.distributed as dist
+        n = ctx.n
+        R, L, C = g.shape
+        send = g.view(R, L, n, C // n).permute(2, 0, 1, 3).contiguous()
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=ctx.group)
+        if ctx.log is not None:
+            ctx.log.record("all_to_all", send.numel(), "ulysses-out-bwd", send.numel() * send.element_size())
+        return recv.view(n * R, L, C // n), None, None, None
+
+
+class HybridStack:
+    """A stack of attention layers following `schedule` (LayerKind FULL / TSA / GSA) on one
+    latent grid `g` (padded internally as anyres.py:57-66).  Input and output: this rank's
+    token-wise shard (G*B, L, C) bf16."""
+
+    def __init__(self, g: GridShape, heads: int, chan: int, schedule=None, num_layers: int = 6,
+                 n_full: int = 2, batch: int = 1, group=None, log: CommLog | None = None,
+                 device=None, seed: int = PROJECTION_SEED):
+        import torch.distributed as dist
+        self.schedule = list(schedule) if schedule is not None else build_layer_schedule(num_layers, n_full)
+        self.g, self.pg = g, pad_grid(g)
+        self.grid = self.pg.padded
+        self.heads, self.chan, self.batch = heads, chan, batch
+        self.group, self.log = group, log
+        self.world = dist.get_world_size(group) if (group is not None or (
+            dist.is_available() and dist.is_initialized())) else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        k2 = g.k * g.k
+        if (k2 * batch) % self.world:
+            raise ValueError(f"{k2 * batch} subsequences do not shard over {self.world} ranks")
+        if any(s is LayerKind.FULL for s in self.schedule) and heads % self.world:
+            raise ValueError(f"full-attention blocks need heads ({heads}) divisible by {self.world}")
+        self.n_sub, self.L = k2, self.grid.seq_len // k2
+        self.local_rows = k2 * batch // self.world
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.weights = [packed_projection(chan, COMPUTE_DTYPE, dev, seed + i)
+                        for i in range(len(self.schedule))]
+        r0 = self.rank * self.local_rows
+        self.bits = {}
+        self.full_bits = {}
+        for pat in (SparsePattern.TOKEN_WISE, SparsePattern.GROUP_WISE):
+            b = self.pg.mask_bits(pat, batch)
+            self.bits[pat] = None if b is None else b[r0:r0 + self.local_rows].contiguous()
+            self.full_bits[pat] = None if b is None else full_sequence_bits(b, k2, batch, self.L)
+        self._t2g = IndexMap._pattern("tsa_to_gsa", self.grid, batch)
+        self._g2t = IndexMap._pattern("gsa_to_tsa", self.grid, batch)
+
+    # ------------------------------------------------------------------ pieces
+    def _switch(self, x, to: SparsePattern):
+        if self.world == 1:
+            return (self._t2g if to is SparsePattern.GROUP_WISE else self._g2t).apply(x)
+        return ssp_switch(x, self.grid, self.group, self.log)
+
+    def _skiparse(self, x, W, pat):
+        qkv = torch.matmul(x, W)
+        bits = self.bits[pat]
+        return attention_packed(qkv, self.heads, bits, zero_invalid_queries=bits is not None)
+
+    def _full(self, x, W, pat):
+        """Full attention over each batch item's whole (padded) sequence, computed in the
+        current pattern layout."""
+        qkv = torch.matmul(x, W)                                  # (R, L, 3C)
+        bits = self.full_bits[pat]
+        n = self.world
+        if n > 1:
+            qkv = _UlyssesQKV.apply(qkv, n, self.group, self.log)  # (k2*B, L, 3C/n)
+        rows, L, C3 = qkv.shape
+        B = self.batch
+        # rows are nested (pattern id, batch item): regroup to one sequence per batch item
+        seq = qkv.view(self.n_sub, B, L, C3).transpose(0, 1).reshape(B, self.n_sub * L, C3)
+        o = attention_packed(seq, self.heads // n, bits, zero_invalid_queries=bits is not None)
+        o = o.view(B, self.n_sub, L, C3 // 3).transpose(0, 1).reshape(rows, L, C3 // 3)
+        if n > 1:
+            o = _UlyssesOut.apply(o, n, self.group, self.log)
+        return o
+
+    def __call__(self, x_tsa: torch.Tensor) -> torch.Tensor:
+        x, layout = x_tsa, SparsePattern.TOKEN_WISE
+        for kind, W in zip(self.schedule, self.weights):
+            if kind is LayerKind.FULL:
+                x = self._full(x, W, layout)
+                continue
+            want = SparsePattern.TOKEN_WISE if kind is LayerKind.TSA else SparsePattern.GROUP_WISE
+            if want is not layout:
+                x = self._switch(x, want)
+                layout = want
+            x = self._skiparse(x, W, layout)
+        if layout is not SparsePattern.TOKEN_WISE:
+            x = self._switch(x, SparsePattern.TOKEN_WISE)
+        return x
+
+    def flops(self) -> dict:
+        d = self.chan // self.heads
+        n_rows = self.local_rows
+        sk = 4 * n_rows * self.L * self.L * d * self.heads
+        S = self.n_sub * self.L
+        full = 4 * self.batch * S * S * d * self.heads // self.world
+        n_full = sum(1 for s in self.schedule if s is LayerKind.FULL)
+        n_sk = len(self.schedule) - n_full
+        return {"attention_fwd": n_full * full + n_sk * sk,
+                "attention_fwd_bwd": 3.5 * (n_full * full + n_sk * sk)}

@@ -114,3 +114,29 @@ def test_comm_comparison_matches_reference_golden(golden_meta):
     from paper_2605_28691_b200 import comm_comparison
     for ref in golden_meta["comm"]:
         assert comm_comparison(ref["group_size"], ref["per_rank_elements"], ref["blocks"]) == ref
+
+
+def test_ospt_and_mask_formats_byte_exact(tmp_path):
+    """OSPT (gridseq.py:232-256) and mask files (anyres.py:99-112) against files the
+    reference wrote (tests/golden/ref_*, made by oracle/make_golden.py)."""
+    import numpy as np
+    import torch
+    from paper_2605_28691_b200 import SequenceTensor, read_ospt, write_ospt
+    from paper_2605_28691_b200 import formats
+    golden = ROOT / "tests" / "golden"
+    x = read_ospt(golden / "ref_x.ospt", device="cpu")
+    want = np.random.Generator(np.random.PCG64(9)).standard_normal((2, 7, 3))
+    assert np.array_equal(x.data.numpy(), want)
+    write_ospt(tmp_path / "x.ospt", x)
+    assert (tmp_path / "x.ospt").read_bytes() == (golden / "ref_x.ospt").read_bytes()
+    with pytest.raises(ValueError):
+        (tmp_path / "bad.ospt").write_bytes(b"NOPE" + bytes(20))
+        read_ospt(tmp_path / "bad.ospt", device="cpu")
+    g, mask = formats.read_mask(golden / "ref_mask_1x5x6_k2.bin")
+    assert (g.t, g.h, g.w, g.k) == (1, 8, 8, 2) and int(mask.sum()) == 30
+
+    class _PG:  # a PaddedGrid-shaped stand-in (the product PaddedGrid needs a GPU mask)
+        padded = g
+    _PG.mask = mask.cpu()
+    formats.write_mask(tmp_path / "m.bin", _PG)
+    assert (tmp_path / "m.bin").read_bytes() == (golden / "ref_mask_1x5x6_k2.bin").read_bytes()

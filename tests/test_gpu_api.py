@@ -270,3 +270,57 @@ def test_block_matches_composed_applications(P):
     want = P.orig_to_tsa(pg.padded).apply(y2)
     err = (y.float() - want.float()).abs().max().item()
     assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("grid,padded", [((2, 12, 16, 2), False), ((2, 10, 12, 2), True)])
+def test_hybrid_stack_matches_layerwise_oracle(P, grid, padded):
+    """HybridStack (FULL, TSA, GSA, TSA, FULL, all in the token-wise layout) equals the
+    reference-semantics composition of skiparse_attention layers in the original layout
+    (ORIGINAL pattern for FULL layers), with the stack's own weights."""
+    from paper_2605_28691_b200.skiparse import LayerKind
+    from paper_2605_28691_b200.stack import HybridStack
+    g = P.GridShape(*grid)
+    og = O.Grid(*grid)
+    C, heads = 256, 2
+    sched = [LayerKind.FULL, LayerKind.TSA, LayerKind.GSA, LayerKind.TSA, LayerKind.FULL]
+    st = HybridStack(g, heads, C, schedule=sched)
+    pgr = O.padded_grid(og)
+    rng = np.random.default_rng(4)
+    x0 = O.bf16_round(rng.standard_normal((1, og.seq_len, C)))
+    x_orig = torch.from_numpy(x0).cuda().to(torch.bfloat16)
+    xt = st.pg.padded  # noqa: F841
+    x_tsa = kernels_rearrange(x_orig, pgr, og)
+    y = st(x_tsa).float().cpu().numpy()
+    # oracle: layer by layer in the original (padded) layout
+    xp = O.pad(x0, og)
+    pat = {LayerKind.FULL: "original", LayerKind.TSA: "tsa", LayerKind.GSA: "gsa"}
+    sim = xp.copy()
+    for kind, W in zip(sched, st.weights):
+        Wd = W.double().cpu().numpy()
+        C_ = W.shape[0]
+        ws = (Wd[:, :C_], Wd[:, C_:2 * C_], Wd[:, 2 * C_:])
+        xp = O.skiparse_attention(xp, og, pat[kind], padded=True, heads=heads, weights=ws)
+        sim = O.skiparse_attention(sim, og, pat[kind], padded=True, heads=heads, weights=ws,
+                                   round_fn=O.bf16_round)
+    tab = O.map_table("orig_to_tsa", pgr, 1)
+    want = O.apply_table(tab, xp)
+    want_sim = O.apply_table(tab, sim)
+    err = np.max(np.abs(y - want))
+    budget = 2 * np.max(np.abs(want_sim - want)) + 1e-2
+    print(f"hybrid stack {grid} padded={padded}: max|err| {err:.3e} budget {budget:.3e}")
+    assert err <= budget
+
+
+def kernels_rearrange(x_orig, pgr, og):
+    from paper_2605_28691_b200 import kernels
+    return kernels.rearrange(x_orig, "orig_to_tsa", pgr.t, pgr.h, pgr.w, pgr.k, 1, og.h, og.w)
+
+
+def test_hybrid_stack_backward_runs(P):
+    from paper_2605_28691_b200.stack import HybridStack
+    g = P.GridShape(2, 10, 12, 2)
+    st = HybridStack(g, 2, 256, num_layers=4, n_full=2)
+    x = torch.randn(st.local_rows, st.L, 256, device="cuda").bfloat16().requires_grad_(True)
+    y = st(x)
+    y.float().sum().backward()
+    assert x.grad is not None and torch.isfinite(x.grad).all()

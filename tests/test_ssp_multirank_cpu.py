@@ -108,3 +108,60 @@ def test_check_switch_guards():
         check_switch(2, 3, 16, g)
     with pytest.raises(ProtocolError):
         check_switch(2, 2, 15, g)
+
+
+def _ulysses_worker(rank, world, port, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2605_28691_b200.stack import _UlyssesOut, _UlyssesQKV
+        R, L, C = 3, 5, 8
+        torch.manual_seed(0)
+        full = torch.randn(world * R, L, 3 * C, dtype=torch.float64)   # all rows, all heads
+        mine = full[rank * R:(rank + 1) * R].clone().requires_grad_(True)
+        heads = _UlyssesQKV.apply(mine, world, None, None)
+        Cn = C // world
+        want = full.view(world * R, L, 3, world, Cn)[:, :, :, rank, :].reshape(world * R, L, 3 * Cn)
+        ok_fwd = torch.equal(heads, want)
+        # adjoint check <f(x), y> == <x, f^T(y)>
+        torch.manual_seed(100 + rank)
+        yb = torch.randn_like(heads)
+        (heads * yb).sum().backward()
+        lhs = torch.tensor([(heads * yb).sum().item()], dtype=torch.float64)
+        rhs = torch.tensor([(mine * mine.grad).sum().item()], dtype=torch.float64)
+        dist.all_reduce(lhs)
+        dist.all_reduce(rhs)
+        ok_adj = torch.allclose(lhs, rhs)
+        # output direction: rows of my heads -> my rows of all heads
+        torch.manual_seed(7)
+        o_all = torch.randn(world * R, L, C, dtype=torch.float64)      # identical on all ranks
+        o_mine_heads = o_all.view(world * R, L, world, Cn)[:, :, rank, :].contiguous().requires_grad_(True)
+        back = _UlyssesOut.apply(o_mine_heads, world, None, None)
+        ok_out = torch.equal(back, o_all[rank * R:(rank + 1) * R])
+        yo = torch.randn_like(back)
+        (back * yo).sum().backward()
+        l2 = torch.tensor([(back * yo).sum().item()], dtype=torch.float64)
+        r2 = torch.tensor([(o_mine_heads * o_mine_heads.grad).sum().item()], dtype=torch.float64)
+        dist.all_reduce(l2)
+        dist.all_reduce(r2)
+        q.put((rank, ok_fwd, ok_adj, ok_out, bool(torch.allclose(l2, r2))))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ulysses_all_to_all_over_gloo(world):
+    """Head-parallel redistribution used by FULL blocks of the hybrid stack: forward
+    gathers all rows for this rank's heads; the backward is the exact adjoint."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ulysses_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert len(r) == 5 and all(r[1:]), r
