@@ -149,6 +149,27 @@ int osp_ssp_unpack(const void* recv, void* dst, int64_t elem_bytes, int64_t chan
                    int64_t group_size, int64_t local_batch, int64_t t, int64_t h, int64_t w,
                    int64_t k, void* stream);
 
+/*
+ * HiF8 codec: replaces hif8.py encode_array / decode_array
+ * (hif8.py:171-193) and the amax / scale of quantize_tensor (hif8.py:223-246).
+ * dtype: 0 = bf16, 1 = fp32, 2 = fp64.  `table` = device pointer to the 256 ascending values
+ * (code 127 = 0).  `scale` (device, nullable = 1.0): element i uses scale[i / scale_group]
+ * (scale_group 0 = one scale).  encode stores code(x * scale) -- nearest value, ties to the
+ * even code, saturating; fp64 inputs are scaled and compared in fp64 (bit-exact with the
+ * reference), bf16/fp32 in fp32.  Non-finite inputs set *nonfinite_flag (device, nullable)
+ * and encode as code 0 (the reference raises EncodeError, hif8.py:174-175).
+ * decode stores table[code] / scale.  osp_absmax: *amax = max |x| (device, NaN propagates).
+ * osp_hif8_scale: scale[i] = target / (amax[i] + eps).
+ */
+int osp_absmax(const void* x, int dtype, int64_t n, double* amax, void* stream);
+int osp_hif8_scale(const double* amax, int64_t count, double target, double eps, double* scale,
+                   void* stream);
+int osp_hif8_encode(const void* x, int dtype, int64_t n, const double* scale,
+                    int64_t scale_group, const double* table, uint8_t* codes, int* nonfinite_flag,
+                    void* stream);
+int osp_hif8_decode(const uint8_t* codes, int64_t n, const double* scale, int64_t scale_group,
+                    const double* table, void* out, int dtype, void* stream);
+
 /* Self-test of the tcgen05 instruction forms (S = A B^T, O = bf16(S) V for one 128-row tile). */
 int osp_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,
                   int64_t head_dim, void* stream);

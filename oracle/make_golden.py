@@ -211,9 +211,32 @@ def formats_golden():
     anyres.write_mask(OUT / "ref_mask_1x5x6_k2.bin", pg)
 
 
+def hif8_golden():
+    """HiF8 codec (hif8.py:77-193) and quantizer (hif8.py:223-246) outputs."""
+    from osp import hif8
+    spec = hif8.DEFAULT_SPEC
+    rng = np.random.Generator(np.random.PCG64(8))
+    vals = spec.values
+    mids = (vals[:-1] + vals[1:]) / 2
+    x = np.concatenate([
+        rng.standard_normal(4000) * 3, rng.standard_normal(2000) * 1e-5,
+        np.geomspace(2.0 ** -24, 1.2 * spec.max_value, 600), -np.geomspace(2.0 ** -24, 1.2 * spec.max_value, 600),
+        vals, mids, np.nextafter(mids, np.inf), np.nextafter(mids, -np.inf), [0.0, -0.0]])
+    arrays = {"values": vals, "x": x, "codes": hif8.encode_array(x), "decoded": hif8.decode_array(np.arange(256))}
+    qx = gridseq.random_tensor(2, 33, 5, seed=3)
+    for mode in ("forward", "backward"):
+        q = hif8.quantize_tensor(qx, mode)
+        arrays[f"q_{mode}_codes"] = q.codes.data
+        arrays[f"q_{mode}_scale"] = np.array([q.scale, q.amax])
+        arrays[f"q_{mode}_deq"] = hif8.dequantize(q).data
+    arrays["q_x"] = qx.data
+    np.savez_compressed(OUT / "hif8.npz", **arrays)
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     formats_golden()
+    hif8_golden()
     a_maps, m_maps = maps_golden()
     np.savez_compressed(OUT / "maps.npz", **a_maps)
     a_pad, m_pad = pad_golden()

@@ -23,10 +23,11 @@ from . import kernels
 from .anyres import PaddedGrid
 from .errors import ShapeError
 from .gridseq import GridShape, SequenceTensor, default_device
-from .skiparse import SparsePattern, inverse_pattern_map, pattern_map
+from .skiparse import SparsePattern, assignment_of, inverse_pattern_map, pattern_map
 
 __all__ = ["PROJECTION_SEED", "qkv_projections", "packed_projection", "project_qkv",
-           "dense_attention", "skiparse_attention", "attention_packed", "FlopReport",
+           "dense_attention", "skiparse_attention", "attention_packed", "masked_dense_attention",
+           "pattern_allow_matrix", "skiparse_reference", "FlopReport",
            "flop_report"]
 
 PROJECTION_SEED = 184594917  # attention.py:20
@@ -201,6 +202,54 @@ def skiparse_attention(x, g: GridShape, pattern: SparsePattern, pg: PaddedGrid |
     if pattern is not SparsePattern.ORIGINAL:
         o = inverse_pattern_map(grid, pattern, B).apply(o)
     out = o.to(xd.dtype)
+    return SequenceTensor(out) if isinstance(x, SequenceTensor) else out
+
+
+def masked_dense_attention(q, k, v, allow):
+    """Dense attention under an explicit 2-D (query, key) permission matrix
+    (attention.py:70-82).  Like the reference this is the ORACLE route -- the production
+    sparse path never builds a 2-D mask -- so it is plain fp64 torch on the device (O(S^2)
+    memory), kept only so reference code that cross-checks skiparse_attention against it
+    keeps running.  Queries with no allowed key output zeros."""
+    qd, kd, vd = _as_tensor(q), _as_tensor(k), _as_tensor(v)
+    a = torch.as_tensor(np.asarray(allow) if not isinstance(allow, torch.Tensor) else allow,
+                        device=qd.device).bool()
+    if a.dim() == 2:
+        a = a.expand(qd.shape[0], qd.shape[1], qd.shape[1])
+    qd, kd, vd = (t.to(torch.float64) for t in (qd, kd, vd))
+    s = torch.einsum("bic,bjc->bij", qd, kd) / math.sqrt(qd.shape[-1])
+    s = s.masked_fill(~a, float("-inf"))
+    m = s.amax(-1, keepdim=True)
+    m = torch.where(torch.isfinite(m), m, torch.zeros_like(m))
+    w = torch.exp(s - m)
+    den = w.sum(-1, keepdim=True)
+    w = torch.where(den > 0, w / torch.where(den == 0, torch.ones_like(den), den), torch.zeros_like(w))
+    out = torch.einsum("bij,bjc->bic", w, vd)
+    return SequenceTensor(out) if isinstance(q, SequenceTensor) else out
+
+
+def pattern_allow_matrix(g: GridShape, pattern: SparsePattern, pg: PaddedGrid | None = None):
+    """(seq, seq) permission: u, v interact iff they share a subsequence under the pattern
+    and, when padded, both are real tokens (attention.py:85-94)."""
+    grid = pg.padded if pg is not None else g
+    sub = assignment_of(grid, pattern).subseq
+    allow = sub[:, None] == sub[None, :]
+    if pg is not None:
+        m = pg.mask.to(sub.device).bool()
+        allow &= m[:, None] & m[None, :]
+    return allow
+
+
+def skiparse_reference(x, g: GridShape, pattern: SparsePattern, pg: PaddedGrid | None = None):
+    """Oracle route (attention.py:134-143): dense attention over the original layout under
+    the 2-D pattern mask, in fp64 with the reference's fp64 projections."""
+    xd = _as_tensor(x)
+    grid = pg.padded if pg is not None else g
+    if xd.shape[1] != grid.seq_len:
+        raise ShapeError(f"expected seq {grid.seq_len}, got {xd.shape[1]}")
+    wq, wk, wv = qkv_projections(xd.shape[-1], device=xd.device)
+    x64 = xd.to(torch.float64)
+    out = masked_dense_attention(x64 @ wq, x64 @ wk, x64 @ wv, pattern_allow_matrix(g, pattern, pg))
     return SequenceTensor(out) if isinstance(x, SequenceTensor) else out
 
 

@@ -47,7 +47,8 @@ def plan_parallel(world: int, k: int) -> tuple[int, int]:
 
 class SkiparseBlock:
     def __init__(self, g: GridShape, heads: int, chan: int, batch: int = 1, group=None,
-                 log: CommLog | None = None, device=None, seeds=(PROJECTION_SEED, PROJECTION_SEED + 1)):
+                 log: CommLog | None = None, device=None, seeds=(PROJECTION_SEED, PROJECTION_SEED + 1),
+                 transport: str = "native"):
         import torch.distributed as dist
         self.g = g
         self.pg: PaddedGrid = pad_grid(g)
@@ -58,6 +59,7 @@ class SkiparseBlock:
             dist.is_available() and dist.is_initialized())) else 1
         self.rank = dist.get_rank(group) if self.world > 1 else 0
         self.log = log
+        self.transport = transport
         n_sub = g.k * g.k
         if (n_sub * batch) % self.world:
             raise ValueError(f"{n_sub * batch} subsequences do not shard over {self.world} ranks")
@@ -78,12 +80,12 @@ class SkiparseBlock:
     def switch_to_gsa(self, x):
         if self.world == 1:
             return self._t2g.apply(x)
-        return ssp_switch(x, self.grid, self.group, self.log)
+        return ssp_switch(x, self.grid, self.group, self.log, self.transport)
 
     def switch_to_tsa(self, x):
         if self.world == 1:
             return self._g2t.apply(x)
-        return ssp_switch(x, self.grid, self.group, self.log)
+        return ssp_switch(x, self.grid, self.group, self.log, self.transport)
 
     def attend(self, x, W, bits):
         qkv = torch.matmul(x, W)

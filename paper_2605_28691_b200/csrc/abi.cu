@@ -18,6 +18,13 @@ int launch_bytes_to_bits(const uint8_t* valid, uint32_t* bits, int64_t n_rows, i
 int launch_bits_to_bytes(const uint32_t* bits, uint8_t* valid, int64_t n_rows, int64_t L,
                          cudaStream_t stream);
 int launch_invert_index(const int64_t* index, int64_t* inv, int64_t n, cudaStream_t stream);
+int launch_hif8_encode(const void* x, int dtype, int64_t n, const double* scale, int64_t group,
+                       const double* table, uint8_t* codes, int* nonfinite, cudaStream_t stream);
+int launch_hif8_decode(const uint8_t* codes, int64_t n, const double* scale, int64_t group,
+                       const double* table, void* out, int dtype, cudaStream_t stream);
+int launch_absmax(const void* x, int dtype, int64_t n, double* out, cudaStream_t stream);
+int launch_hif8_scale(const double* amax, int64_t count, double target, double eps, double* scale,
+                      cudaStream_t stream);
 
 static thread_local std::string g_err;
 
@@ -346,6 +353,43 @@ int osp_ssp_unpack(const void* recv, void* dst, int64_t elem_bytes, int64_t chan
   if (rc != kOk) return rc;
   const int64_t L = t * h * w / (k * k);
   return launch_permute(p, recv, dst, local_batch * L, elem_bytes * chan, as_stream(stream));
+}
+
+int osp_absmax(const void* x, int dtype, int64_t n, double* amax, void* stream) {
+  if (n < 0) {
+    set_error("negative size");
+    return kValue;
+  }
+  return launch_absmax(x, dtype, n, amax, as_stream(stream));
+}
+
+int osp_hif8_scale(const double* amax, int64_t count, double target, double eps, double* scale,
+                   void* stream) {
+  if (count < 1) {
+    set_error("scale count must be positive");
+    return kValue;
+  }
+  return launch_hif8_scale(amax, count, target, eps, scale, as_stream(stream));
+}
+
+int osp_hif8_encode(const void* x, int dtype, int64_t n, const double* scale,
+                    int64_t scale_group, const double* table, uint8_t* codes, int* nonfinite_flag,
+                    void* stream) {
+  if (n < 0 || scale_group < 0 || !table) {
+    set_error("hif8 encode: bad size / group / missing value table");
+    return kValue;
+  }
+  return launch_hif8_encode(x, dtype, n, scale, scale_group, table, codes, nonfinite_flag,
+                            as_stream(stream));
+}
+
+int osp_hif8_decode(const uint8_t* codes, int64_t n, const double* scale, int64_t scale_group,
+                    const double* table, void* out, int dtype, void* stream) {
+  if (n < 0 || scale_group < 0 || !table) {
+    set_error("hif8 decode: bad size / group / missing value table");
+    return kValue;
+  }
+  return launch_hif8_decode(codes, n, scale, scale_group, table, out, dtype, as_stream(stream));
 }
 
 int osp_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,

@@ -246,3 +246,56 @@ def debug_mma(a: torch.Tensor, b: torch.Tensor, v: torch.Tensor):
 
 def softmax_scale(d: int) -> float:
     return 1.0 / math.sqrt(d)
+
+
+# ----------------------------------------------------------------------------- HiF8
+DTYPE_IDS = {torch.bfloat16: 0, torch.float32: 1, torch.float64: 2}
+
+
+def absmax(x: torch.Tensor) -> torch.Tensor:
+    """max |x| as a 1-element float64 device tensor (no host sync)."""
+    L = _lib.lib()
+    _cuda(x, "x")
+    x = x.contiguous()
+    out = torch.empty(1, dtype=torch.float64, device=x.device)
+    _lib.check(STATS.run("hif8", 1, lambda: L.osp_absmax(x.data_ptr(), DTYPE_IDS[x.dtype], x.numel(),
+                                                          out.data_ptr(), _lib.stream_ptr(x.device))))
+    return out
+
+
+def hif8_scale(amax: torch.Tensor, target: float, eps: float) -> torch.Tensor:
+    L = _lib.lib()
+    scale = torch.empty_like(amax)
+    _lib.check(STATS.run("hif8", 1, lambda: L.osp_hif8_scale(amax.data_ptr(), amax.numel(), target, eps,
+                                                              scale.data_ptr(), _lib.stream_ptr(amax.device))))
+    return scale
+
+
+def hif8_encode(x: torch.Tensor, table: torch.Tensor, scale: torch.Tensor | None = None,
+                scale_group: int = 0, check_finite: bool = True) -> torch.Tensor:
+    L = _lib.lib()
+    _cuda(x, "x")
+    x = x.contiguous()
+    if x.dtype not in DTYPE_IDS:
+        raise UnsupportedError(f"hif8 encode supports bf16/fp32/fp64, got {x.dtype}")
+    codes = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=x.device) if check_finite else None
+    _lib.check(STATS.run("hif8", 1, lambda: L.osp_hif8_encode(
+        x.data_ptr(), DTYPE_IDS[x.dtype], x.numel(), _lib.ptr(scale), scale_group, table.data_ptr(),
+        codes.data_ptr(), _lib.ptr(flag), _lib.stream_ptr(x.device))))
+    if check_finite and int(flag.item()):
+        from .hif8 import EncodeError
+        raise EncodeError("cannot encode non-finite values")
+    return codes
+
+
+def hif8_decode(codes: torch.Tensor, table: torch.Tensor, dtype=torch.float64,
+                scale: torch.Tensor | None = None, scale_group: int = 0) -> torch.Tensor:
+    L = _lib.lib()
+    _cuda(codes, "codes")
+    codes = codes.contiguous()
+    out = torch.empty(codes.shape, dtype=dtype, device=codes.device)
+    _lib.check(STATS.run("hif8", 1, lambda: L.osp_hif8_decode(
+        codes.data_ptr(), codes.numel(), _lib.ptr(scale), scale_group, table.data_ptr(), out.data_ptr(),
+        DTYPE_IDS[dtype], _lib.stream_ptr(codes.device))))
+    return out

@@ -190,37 +190,67 @@ def comm_comparison(group_size: int, per_rank_elements: int, blocks: int = 1,
 
 # ----------------------------------------------------------------------------- multi-process
 
-def _dist_switch(x: torch.Tensor, g: GridShape, group, log: CommLog | None) -> torch.Tensor:
+def _dist_switch(x: torch.Tensor, g: GridShape, group, log: CommLog | None,
+                 transport: str = "native", mode: str = "forward") -> torch.Tensor:
     import torch.distributed as dist
     n = dist.get_world_size(group)
     local_batch, seq, chan = x.shape
     check_switch(n, local_batch, seq, g)
     send = kernels.ssp_pack(x, n, g.t, g.h, g.w, g.k)
-    recv = torch.empty_like(send)
-    if n == 1:
-        recv = send
+    if transport == "hif8":
+        # 8-bit transport: per-rank current scaling of the send
+        # buffer (hif8.py:223-246), one all-to-all of codes, every rank's scale all-gathered,
+        # each received chunk decoded with its source rank's scale.
+        from .hif8 import BACKWARD_MAX, DEFAULT_EPS, DEFAULT_SPEC, FORWARD_MAX
+        table = DEFAULT_SPEC.device_table(x.device)
+        amax = kernels.absmax(send)
+        scale = kernels.hif8_scale(amax, FORWARD_MAX if mode == "forward" else BACKWARD_MAX,
+                                   DEFAULT_EPS)
+        codes = kernels.hif8_encode(send, table, scale, check_finite=False)
+        scales = torch.empty(n, dtype=scale.dtype, device=scale.device)
+        rcodes = torch.empty_like(codes)
+        if n == 1:
+            scales.copy_(scale)
+            rcodes = codes
+        else:
+            dist.all_gather_into_tensor(scales, scale, group=group)
+            dist.all_to_all_single(rcodes, codes, group=group)
+        if log is not None:
+            log.record("all_to_all", codes.numel(), "pattern-switch-hif8", codes.numel())
+        recv = kernels.hif8_decode(rcodes, table, send.dtype, scales, codes.numel() // n)
+    elif transport == "native":
+        recv = torch.empty_like(send)
+        if n == 1:
+            recv = send
+        else:
+            dist.all_to_all_single(recv, send, group=group)
+        if log is not None:
+            log.record("all_to_all", send.numel(), "pattern-switch", send.numel() * send.element_size())
     else:
-        dist.all_to_all_single(recv, send, group=group)
-    if log is not None:
-        log.record("all_to_all", send.numel(), "pattern-switch", send.numel() * send.element_size())
+        raise ValueError(f"unknown transport {transport!r}")
     return kernels.ssp_unpack(recv, n, local_batch, g.t, g.h, g.w, g.k)
 
 
 class SSPSwitch(torch.autograd.Function):
     """One rank's TSA<->GSA switch over a torch.distributed group; the backward
-    is the same switch (the routine is its own inverse, ssp.py:142-144)."""
+    is the same switch (the routine is its own inverse, ssp.py:142-144).  With the
+    HiF8 transport the forward uses forward-mode scaling and the backward
+    backward-mode scaling (hif8.py:47-52)."""
 
     @staticmethod
-    def forward(ctx, x, g, group, log):
-        ctx.g, ctx.group, ctx.log = g, group, log
-        return _dist_switch(x.contiguous(), g, group, log)
+    def forward(ctx, x, g, group, log, transport):
+        ctx.g, ctx.group, ctx.log, ctx.transport = g, group, log, transport
+        return _dist_switch(x.contiguous(), g, group, log, transport, "forward")
 
     @staticmethod
     def backward(ctx, gy):
-        return _dist_switch(gy.contiguous(), ctx.g, ctx.group, ctx.log), None, None, None
+        return (_dist_switch(gy.contiguous(), ctx.g, ctx.group, ctx.log, ctx.transport, "backward"),
+                None, None, None, None)
 
 
-def ssp_switch(x: torch.Tensor, g: GridShape, group=None, log: CommLog | None = None) -> torch.Tensor:
+def ssp_switch(x: torch.Tensor, g: GridShape, group=None, log: CommLog | None = None,
+               transport: str = "native") -> torch.Tensor:
     """Switch this rank's (G*b, L, C) shard between token-wise and group-wise
-    layouts with one NCCL all-to-all (g = padded global grid)."""
-    return SSPSwitch.apply(x, g, group, log)
+    layouts with one NCCL all-to-all (g = padded global grid).  transport="hif8"
+    moves 8-bit HiF8 codes instead of the native dtype (half of bf16's bytes)."""
+    return SSPSwitch.apply(x, g, group, log, transport)

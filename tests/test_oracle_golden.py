@@ -170,3 +170,20 @@ def test_bf16_round():
     import torch
     want = torch.tensor(x, dtype=torch.float64).to(torch.bfloat16).to(torch.float64).numpy()
     assert np.array_equal(r, want)
+
+
+def test_hif8_oracle_matches_reference(golden):
+    from oracle import hif8_oracle as H
+    h = golden("hif8")
+    vals = H.value_table()
+    assert np.array_equal(vals, h["values"])
+    assert len(set(vals.tolist())) == 256 and vals[127] == 0.0
+    assert np.array_equal(H.encode(h["x"]), h["codes"])
+    assert np.array_equal(H.decode(np.arange(256)), h["decoded"])
+    for mode in ("forward", "backward"):
+        codes, scale, amax = H.quantize(h["q_x"], mode)
+        assert np.array_equal(codes, h[f"q_{mode}_codes"])
+        assert (scale, amax) == tuple(h[f"q_{mode}_scale"])
+        assert np.array_equal(H.decode(codes) / scale, h[f"q_{mode}_deq"])
+    with pytest.raises(ValueError):
+        H.encode(np.array([np.inf]))
