@@ -173,6 +173,24 @@ def run_reference(args, world, rank):
 
 # ----------------------------------------------------------------------------- GPU leg
 
+def _ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
+    `ncu --set full` capture of this kernel at cfg3 (profiles/r*_ncu_<kernel>_summary.txt,
+    newest round first)."""
+    import glob
+    import re
+    files = sorted(glob.glob(str(Path(__file__).resolve().parent / "profiles" / f"r*_ncu_{kernel}_summary.txt")))
+    if not files:
+        return None, None
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    for line in Path(files[-1]).read_text().splitlines():
+        m = re.match(r"dram__bytes_(read|write)\.sum = ([0-9.]+) (\w+)", line)
+        if m:
+            total += float(m.group(2)) * units.get(m.group(3), 1)
+    return (total or None), f"{Path(files[-1]).name} (one cold ncu replay, bytes per launch)"
+
+
 def run_ours(args, world, rank, local_rank):
     import torch
     import torch.distributed as dist
@@ -311,6 +329,11 @@ def run_ours(args, world, rank, local_rank):
             "block_tensor_tflops_per_gpu": total_tflops,
             "block_frac_of_peak": total_tflops / sustained,
             "block_frac_of_burst_peak": total_tflops / burst}
+    traffic, tsrc = _ncu_traffic("attn_bwd_v2") if (args.config == "cfg3" and world == 1) else (None, None)
+    roof["traffic"] = traffic
+    roof["traffic_source"] = tsrc
+    ftraffic, _ = _ncu_traffic("attn_fwd") if (args.config == "cfg3" and world == 1) else (None, None)
+    roof["fwd_kernel"]["traffic"] = ftraffic
     share = {n: v["total_ms"] / ms for n, v in kern.items()}
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
