@@ -223,7 +223,27 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
     float m_used = -INFINITY;
     float l = 0.f;
+    // key-mask words of tile j (validity bits and the subsequence tail), fetched one tile ahead
+    auto mask_words = [&](int j, uint32_t (&w)[4]) {
+      const int kv0 = j * kBN;
+      const int nvalid = min(kBN, a.seq_len - kv0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t m = vbits ? ((kv0 >> 5) + i < a.words_per_seq ? __ldg(vbits + (kv0 >> 5) + i) : 0u)
+                           : 0xFFFFFFFFu;
+        const int lo = i * 32;
+        if (nvalid <= lo) m = 0u;
+        else if (nvalid < lo + 32) m &= (1u << (nvalid - lo)) - 1u;
+        w[i] = m;
+      }
+    };
+    uint32_t w_next[4];
+    mask_words(0, w_next);
     for (int j = 0; j < a.n_kv; ++j) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w[i] = w_next[i];
+      if (j + 1 < a.n_kv) mask_words(j + 1, w_next);
       mbar_wait(bar_s + t, j & 1);
       tc_fence_after();
       if (a.flags & 2) {
@@ -236,20 +256,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int cc = 0; cc < 4; ++cc) tmem_ld32(tS + cc * 32, s[cc]);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) tmem_wait_ld(s[cc]);
-
-      // key mask: validity bits and the subsequence tail
-      const int kv0 = j * kBN;
-      const int nvalid = min(kBN, a.seq_len - kv0);
-      uint32_t w[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        uint32_t m = vbits ? ((kv0 >> 5) + i < a.words_per_seq ? __ldg(vbits + (kv0 >> 5) + i) : 0u)
-                           : 0xFFFFFFFFu;
-        const int lo = i * 32;
-        if (nvalid <= lo) m = 0u;
-        else if (nvalid < lo + 32) m &= (1u << (nvalid - lo)) - 1u;
-        w[i] = m;
-      }
       if ((w[0] & w[1] & w[2] & w[3]) != 0xFFFFFFFFu) {
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc)
@@ -257,18 +263,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int i = 0; i < 32; ++i)
             if (!((w[cc] >> i) & 1u)) s[cc][i] = __float_as_uint(-INFINITY);
       }
-      float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        mx0 = fmaxf(mx0, __uint_as_float(s[0][i]));
-        mx1 = fmaxf(mx1, __uint_as_float(s[1][i]));
-        mx2 = fmaxf(mx2, __uint_as_float(s[2][i]));
-        mx3 = fmaxf(mx3, __uint_as_float(s[3][i]));
-      }
-      const float m_new = fmaxf(m_used, fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)));
-      const bool need = (m_new > m_used) &&
-                        (m_used == -INFINITY || (m_new - m_used) * c > kRescaleThreshold);
-      if (__any_sync(0xFFFFFFFFu, need)) {
+      // Rescale O (in TMEM) and l to a new running max.  PV_{j-1} of this tile is complete:
+      // S_j was committed after it and tcgen05 operations execute in order.
+      auto rescale = [&](float m_new) {
         const float m_upd = fmaxf(m_new, m_used);
         const float alpha = (m_used == -INFINITY) ? 0.f : ex2((m_used - m_upd) * c);
         if (j > 0) {
@@ -284,28 +281,65 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         l *= alpha;
         m_used = m_upd;
-      }
-      const float ms = (m_used == -INFINITY) ? 0.f : m_used * c;
-      float ls0 = 0.f, ls1 = 0.f;
-      named_bar_sync(my_turn, 256);
+      };
+      auto row_max = [&]() {
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float p0 = fmaf(__uint_as_float(s[cc][2 * i]), c, -ms);
-          float p1 = fmaf(__uint_as_float(s[cc][2 * i + 1]), c, -ms);
-          if (!(a.flags & 1)) {
-            p0 = ex2(p0);
-            p1 = ex2(p1);
-          }
-          ls0 += p0;
-          ls1 += p1;
-          pk[i] = pack_bf16(p0, p1);
+        for (int i = 0; i < 32; ++i) {
+          mx0 = fmaxf(mx0, __uint_as_float(s[0][i]));
+          mx1 = fmaxf(mx1, __uint_as_float(s[1][i]));
+          mx2 = fmaxf(mx2, __uint_as_float(s[2][i]));
+          mx3 = fmaxf(mx3, __uint_as_float(s[3][i]));
         }
-        if (cc == 3 && !(t == 1 && j == a.n_kv - 1))
-          asm volatile("bar.arrive %0, 256;" ::"r"(next_turn) : "memory");
-        tmem_st16(tS + cc * 16, pk);
+        return fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+      };
+      auto needs_rescale = [&](float m_new) {
+        return (m_new > m_used) && (m_used == -INFINITY || (m_new - m_used) * c > kRescaleThreshold);
+      };
+      // exp2 of the tile against the current max, P -> TMEM (bf16 over the S columns)
+      float ls0 = 0.f, ls1 = 0.f;
+      auto exps = [&](bool turn) {
+        const float ms = (m_used == -INFINITY) ? 0.f : m_used * c;
+        ls0 = 0.f;
+        ls1 = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float p0 = fmaf(__uint_as_float(s[cc][2 * i]), c, -ms);
+            float p1 = fmaf(__uint_as_float(s[cc][2 * i + 1]), c, -ms);
+            if (!(a.flags & 1)) {
+              p0 = ex2(p0);
+              p1 = ex2(p1);
+            }
+            ls0 += p0;
+            ls1 += p1;
+            pk[i] = pack_bf16(p0, p1);
+          }
+          if (turn && cc == 3 && !(t == 1 && j == a.n_kv - 1))
+            asm volatile("bar.arrive %0, 256;" ::"r"(next_turn) : "memory");
+          tmem_st16(tS + cc * 16, pk);
+        }
+      };
+      if (__any_sync(0xFFFFFFFFu, m_used == -INFINITY)) {
+        // no running max yet: exact row max first
+        const float m_new = fmaxf(m_used, row_max());
+        if (__any_sync(0xFFFFFFFFu, needs_rescale(m_new))) rescale(m_new);
+        named_bar_sync(my_turn, 256);
+        exps(true);
+      } else {
+        // Speculative: exponentiate against the running max straight away (values up to 2^8
+        // above it are fine for bf16 P and the fp32 sums -- the lazy-rescale threshold) while
+        // the row max is reduced off the MUFU critical path; a tile that overshoots by more is
+        // rescaled and redone (rare once the max has settled).
+        named_bar_sync(my_turn, 256);
+        exps(true);
+        const float m_new = fmaxf(m_used, row_max());
+        if (__any_sync(0xFFFFFFFFu, needs_rescale(m_new))) {
+          rescale(m_new);
+          exps(false);
+        }
       }
       tmem_wait_st();
       l += ls0 + ls1;
