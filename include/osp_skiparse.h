@@ -170,6 +170,25 @@ int osp_hif8_encode(const void* x, int dtype, int64_t n, const double* scale,
 int osp_hif8_decode(const uint8_t* codes, int64_t n, const double* scale, int64_t scale_group,
                     const double* table, void* out, int dtype, void* stream);
 
+/*
+ * K6: QKV projection with the QK-RMSNorm + 3-D RoPE prologue; with
+ * norm = 0 and rope_table = NULL it is the reference's fixed projection (attention.py:20-32).
+ *   x     : (rows, chan) bf16, rows in the pattern layout `pattern` (0 original, 1 TSA, 2 GSA)
+ *           of `batch` items on the padded grid (t, h, w, k)
+ *   w_t   : (3*chan, chan) bf16 = [Wq | Wk | Wv]^T (K-major)
+ *   out   : (rows, >= 3*chan) bf16 q | k | v, row stride out_stride (elements)
+ *   norm  : 0 none; 1 RMSNorm over each 128-channel head of q and k; 2 RMSNorm of q and k over
+ *           all chan channels (needs sumsq, (rows, 2) fp32 workspace); gamma_q / gamma_k (chan)
+ *           fp32 or NULL (= 1)
+ *   rope_table: NULL or (t + h + w, 32) float2 (cos, sin) per axis position and pair; head pairs
+ *           (2i, 2i+1) split over (t, h, w) as 22 / 21 / 21 (Wan 3-D RoPE for head_dim 128)
+ * head_dim is 128 (chan % 128 == 0).
+ */
+int osp_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, int64_t chan,
+                    int64_t out_stride, int norm, const float* gamma_q, const float* gamma_k,
+                    float eps, float* sumsq, const float* rope_table, int64_t t, int64_t h,
+                    int64_t w, int64_t k, int pattern, int64_t batch, void* stream);
+
 /* Self-test of the tcgen05 instruction forms (S = A B^T, O = bf16(S) V for one 128-row tile). */
 int osp_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,
                   int64_t head_dim, void* stream);

@@ -1,0 +1,403 @@
+// K6: QKV projection with the QK-RMSNorm + 3-D RoPE prologue of the attention (SURVEY.md sec. 8f
+// row 2) on sm_100a -- one tcgen05 GEMM whose epilogue writes the attention-ready q | k | v in the
+// pattern layout.
+//
+//   out[r, :] = x[r, :] @ W          x: (rows, C) bf16 in the pattern layout (rows = k^2*B*L)
+//                                    W: given as W^T (3C, C) bf16, K-major
+//   q, k columns ([0, 2C)), per 128-wide head:
+//     norm 1 (per head):   v *= rsqrt(mean_head(v^2) + eps) * gamma[c]
+//     norm 2 (per token over all C channels, Wan-style): the epilogue writes bf16 v and adds the
+//                          row's sum of squares into `sumsq`; qk_norm_rope_kernel then scales and
+//                          rotates in place
+//     rope:                pairs (2i, 2i+1) of each head rotated by pos_axis(i) * freq(i); the
+//                          64 pairs split over (t, h, w) as (d - 4*(d/6), 2*(d/6), 2*(d/6)) / 2;
+//                          positions are the token's padded-grid coordinates, recovered in closed
+//                          form from its pattern-layout row (skiparse.py:68-114 inverted).
+// The reference's projection (attention.py:20-32) is this GEMM with norm 0 and rope off.
+//
+// Kernel: persistent, clusters of two CTAs (one per SM) on vertically adjacent 128 x 256 output
+// tiles that share their 256 x 64 weight slice per K step: each CTA loads its own x rows and
+// half of the weight slice, TMA-multicast into both CTAs (half the L2 -> SM traffic of W; the
+// shape cuBLAS uses for this GEMM).  64-deep K steps through a 4-stage ring (128B swizzle); a
+// stage is refilled once BOTH CTAs' MMAs have read it (multicast tcgen05.commit).  tcgen05.mma
+// M=128 N=256 issued by one thread; two 256-column TMEM accumulators so the epilogue of tile i
+// overlaps the main loop of tile i+1.  Tile pairs are visited in bands of 16 pairs (32 row tiles,
+// 42 MB of x at C=5120) across all column tiles, so each band of x stays in L2 while the
+// weights stream through it once per band.
+#include "osp_common.cuh"
+#include "osp_internal.h"
+
+namespace osp {
+namespace {
+
+constexpr int kPBM = 128, kPBN = 256, kPBK = 64, kPStages = 4, kPBand = 16;  // band in tile pairs
+constexpr int kPThreads = 256;
+
+struct ProjLayout {
+  static constexpr int kA = 0;                                   // stages x 16 KB
+  static constexpr int kB = kPStages * kPBM * kPBK * 2;          // stages x 32 KB
+  static constexpr int kBar = kB + kPStages * kPBN * kPBK * 2;
+  static constexpr int kSmem = kBar + 256;
+};
+
+struct ProjArgs {
+  __nv_bfloat16* out;
+  int64_t out_stride;
+  int rows, chan, n_cols, n_pairs_m, n_tiles_n, k_steps;
+  int norm;                 // 0 none, 1 per head, 2 per token (two-phase)
+  const float* gamma_q;     // (C) or null
+  const float* gamma_k;
+  float eps;
+  float* sumsq;             // (rows, 2) for norm 2
+  const float2* rope;       // (T + H + W, 32) cos/sin, or null
+  int pattern;              // 0 original, 1 TSA, 2 GSA
+  int B, T, H, W, k, L;     // padded grid, batch, subsequence length
+  int d_t, d_h;             // pairs on the t and h axes (the rest on w)
+};
+
+// Padded-grid (t, h, w) of pattern-layout row `r` (inverse of skiparse.py:68-114).
+__device__ __forceinline__ void row_coords(const ProjArgs& a, int r, int& t, int& h, int& w) {
+  if (a.pattern == 0) {
+    const int pos = r % (a.T * a.H * a.W);
+    w = pos % a.W;
+    h = (pos / a.W) % a.H;
+    t = pos / (a.W * a.H);
+    return;
+  }
+  const int s = r / a.L, pos = r % a.L;
+  const int pq = s / a.B;
+  const int p = pq / a.k, q = pq % a.k;
+  if (a.pattern == 1) {
+    const int hk = a.H / a.k, wk = a.W / a.k;
+    const int ww = pos % wk, hh = (pos / wk) % hk;
+    t = pos / (wk * hk);
+    h = hh * a.k + p;
+    w = ww * a.k + q;
+  } else {
+    const int k2 = a.k * a.k;
+    const int hk2 = a.H / k2, wk2 = a.W / k2;
+    const int q2 = pos % a.k;
+    const int x = pos / a.k;
+    const int wg = x % wk2;
+    const int y = x / wk2;
+    const int p2 = y % a.k;
+    const int txh = y / a.k;
+    const int hg = txh % hk2;
+    t = txh / hk2;
+    h = hg * k2 + p * a.k + p2;
+    w = wg * k2 + q * a.k + q2;
+  }
+}
+
+// Normalise (norm 1) and rotate one 128-channel head held by this thread.
+__device__ __forceinline__ void head_epilogue(float (&v)[128], const ProjArgs& a, const float* gamma,
+                                              int c0, int t, int h, int w, bool rope) {
+  if (a.norm == 1) {
+    float ss0 = 0.f, ss1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 128; i += 2) {
+      ss0 = fmaf(v[i], v[i], ss0);
+      ss1 = fmaf(v[i + 1], v[i + 1], ss1);
+    }
+    const float r = rsqrtf((ss0 + ss1) * (1.f / 128.f) + a.eps);
+#pragma unroll
+    for (int i = 0; i < 128; ++i) v[i] *= r * (gamma ? __ldg(gamma + (c0 + i)) : 1.f);
+  }
+  if (rope) {
+    const float2* rt = a.rope + static_cast<int64_t>(t) * 32;
+    const float2* rh = a.rope + static_cast<int64_t>(a.T + h) * 32;
+    const float2* rw = a.rope + static_cast<int64_t>(a.T + a.H + w) * 32;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      const float2 cs = i < a.d_t ? __ldg(rt + i) : (i < a.d_t + a.d_h ? __ldg(rh + (i - a.d_t))
+                                                                         : __ldg(rw + (i - a.d_t - a.d_h)));
+      const float x0 = v[2 * i], x1 = v[2 * i + 1];
+      v[2 * i] = x0 * cs.x - x1 * cs.y;
+      v[2 * i + 1] = x0 * cs.y + x1 * cs.x;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPThreads, 1)
+    qkv_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const ProjArgs a) {
+  using Ly = ProjLayout;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Ly::kBar);
+  uint64_t* bar_full = bars;                  // [stages] TMA -> MMA
+  uint64_t* bar_empty = bars + kPStages;      // [stages] MMA -> TMA
+  uint64_t* bar_acc = bars + 2 * kPStages;    // [2] MMA -> epilogue
+  uint64_t* bar_accf = bars + 2 * kPStages + 2;  // [2] epilogue -> MMA (128 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kPStages + 4);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const int n_units = a.n_pairs_m * a.n_tiles_n;  // a unit = two vertically adjacent tiles
+  auto tile_mn = [&](int id, int& tm, int& tn) {
+    const int band_units = kPBand * a.n_tiles_n;
+    const int band = id / band_units;
+    const int rem = id % band_units;
+    const int pairs_in_band = min(kPBand, a.n_pairs_m - band * kPBand);
+    tm = 2 * (band * kPBand + rem % pairs_in_band) + static_cast<int>(crank);
+    tn = rem / pairs_in_band;
+  };
+
+  if ((smem_u32(sm) & 1023) != 0) __trap();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPStages; ++i) {
+      mbar_init(bar_full + i, 1);
+      mbar_init(bar_empty + i, 2);  // both CTAs' MMAs read the multicast W half
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_acc + i, 1);
+      mbar_init(bar_accf + i, 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch(&tmA);
+      tma_prefetch(&tmB);
+      int it = 0;
+      for (int id = cluster; id < n_units; id += n_clusters) {
+        int tm, tn;
+        tile_mn(id, tm, tn);
+        for (int ks = 0; ks < a.k_steps; ++ks, ++it) {
+          const int st = it % kPStages;
+          mbar_wait(bar_empty + st, ((it / kPStages) & 1) ^ 1);
+          mbar_expect_tx(bar_full + st, (kPBM + kPBN) * kPBK * 2);
+          tma_load_3d(sm + Ly::kA + st * kPBM * kPBK * 2, &tmA, bar_full + st, ks * kPBK, tm * kPBM, 0);
+          // my half of the shared W slice, delivered to both CTAs
+          tma_load_3d_multicast(sm + Ly::kB + st * kPBN * kPBK * 2 + crank * (kPBN / 2) * kPBK * 2, &tmB,
+                                bar_full + st, ks * kPBK, tn * kPBN + static_cast<int>(crank) * (kPBN / 2), 0,
+                                0x3);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    constexpr uint32_t kId = idesc_bf16(kPBM, kPBN, 0, 0);
+    if (elect_one()) {
+      int it = 0, lt = 0;
+      for (int id = cluster; id < n_units; id += n_clusters, ++lt) {
+        const int buf = lt & 1;
+        if (lt >= 2) mbar_wait(bar_accf + buf, ((lt >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * kPBN;
+        for (int ks = 0; ks < a.k_steps; ++ks, ++it) {
+          const int st = it % kPStages;
+          mbar_wait(bar_full + st, (it / kPStages) & 1);
+          tc_fence_after();
+          const uint32_t ab = smem_u32(sm + Ly::kA + st * kPBM * kPBK * 2);
+          const uint32_t bb = smem_u32(sm + Ly::kB + st * kPBN * kPBK * 2);
+#pragma unroll
+          for (int kk = 0; kk < kPBK / 16; ++kk)
+            mma_ss(acc, sdesc_sw128(ab + kk * 32, 16, 1024), sdesc_sw128(bb + kk * 32, 16, 1024), kId,
+                   (ks > 0 || kk > 0) ? 1u : 0u);
+          tc_commit_multicast(bar_empty + st, 0x3);
+        }
+        tc_commit(bar_acc + buf);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogue (thread = row)
+    const int wq = warp & 3;
+    const uint32_t la = static_cast<uint32_t>(wq * 32) << 16;
+    int lt = 0;
+    for (int id = cluster; id < n_units; id += n_clusters, ++lt) {
+      int tm, tn;
+      tile_mn(id, tm, tn);
+      const int buf = lt & 1;
+      mbar_wait(bar_acc + buf, (lt >> 1) & 1);
+      tc_fence_after();
+      const int row = tm * kPBM + wq * 32 + lane;
+      const bool row_ok = row < a.rows;
+      int t = 0, h = 0, w = 0;
+      if (a.rope) row_coords(a, row_ok ? row : 0, t, h, w);
+      for (int hc = 0; hc < kPBN / 128; ++hc) {
+        float v[128];
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t r[32];
+          tmem_ld32(tmem + la + buf * kPBN + hc * 128 + cc * 32, r);
+          tmem_wait_ld(r);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[cc * 32 + i] = __uint_as_float(r[i]);
+        }
+        if (hc == kPBN / 128 - 1) {
+          tc_fence_before();
+          mbar_arrive(bar_accf + buf);
+        }
+        const int c0 = tn * kPBN + hc * 128;          // first output column of this head
+        if (c0 >= a.n_cols) continue;                 // partial last column tile (3C % 256 == 128)
+        const bool is_q = c0 < a.chan, is_k = !is_q && c0 < 2 * a.chan;
+        if (is_q || is_k) {
+          if (a.norm == 2 && row_ok) {
+            float ss = 0.f;
+#pragma unroll
+            for (int i = 0; i < 128; ++i) {
+              const float b = __bfloat162float(__float2bfloat16(v[i]));
+              ss = fmaf(b, b, ss);
+            }
+            atomicAdd(a.sumsq + static_cast<int64_t>(row) * 2 + (is_q ? 0 : 1), ss);
+          } else {
+            head_epilogue(v, a, is_q ? a.gamma_q : a.gamma_k, is_q ? c0 : c0 - a.chan, t, h, w,
+                          a.rope != nullptr);
+          }
+        }
+        if (row_ok) {
+          uint4* dst = reinterpret_cast<uint4*>(a.out + static_cast<int64_t>(row) * a.out_stride + c0);
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            dst[j] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                                pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // the peer may still multicast into / arrive on this CTA until it is done
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// Second phase of norm 2: q, k rows scaled by rsqrt(mean over C + eps) * gamma, then RoPE.
+// One warp per (row, q|k), each lane owns 4 heads' worth of channel pairs in turn.
+__global__ void __launch_bounds__(256) qk_norm_rope_kernel(ProjArgs a) {
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= static_cast<int64_t>(a.rows) * 2) return;
+  const int row = static_cast<int>(gw >> 1);
+  const int which = static_cast<int>(gw & 1);
+  const float r = rsqrtf(a.sumsq[static_cast<int64_t>(row) * 2 + which] / a.chan + a.eps);
+  const float* gamma = which == 0 ? a.gamma_q : a.gamma_k;
+  int t = 0, h = 0, w = 0;
+  if (a.rope) row_coords(a, row, t, h, w);
+  __nv_bfloat162* base = reinterpret_cast<__nv_bfloat162*>(a.out + static_cast<int64_t>(row) * a.out_stride +
+                                                           static_cast<int64_t>(which) * a.chan);
+  for (int pidx = lane; pidx < a.chan / 2; pidx += 32) {
+    const int c = 2 * pidx;
+    const float2 x = __bfloat1622float2(base[pidx]);
+    float x0 = x.x * r * (gamma ? __ldg(gamma + c) : 1.f);
+    float x1 = x.y * r * (gamma ? __ldg(gamma + c + 1) : 1.f);
+    if (a.rope) {
+      const int i = pidx & 63;  // pair within the head
+      const float2 cs = i < a.d_t ? a.rope[static_cast<int64_t>(t) * 32 + i]
+                                  : (i < a.d_t + a.d_h ? a.rope[static_cast<int64_t>(a.T + h) * 32 + (i - a.d_t)]
+                                                       : a.rope[static_cast<int64_t>(a.T + a.H + w) * 32 +
+                                                                (i - a.d_t - a.d_h)]);
+      const float y0 = x0 * cs.x - x1 * cs.y;
+      const float y1 = x0 * cs.y + x1 * cs.x;
+      x0 = y0;
+      x1 = y1;
+    }
+    base[pidx] = __floats2bfloat162_rn(x0, x1);
+  }
+}
+
+}  // namespace
+
+int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, int64_t chan,
+                       int64_t out_stride, int norm, const float* gamma_q, const float* gamma_k,
+                       float eps, float* sumsq, const float* rope_table, int64_t t, int64_t h,
+                       int64_t w, int64_t k, int pattern, int64_t batch, cudaStream_t stream) {
+  if (chan % 128 != 0 || chan < 128) {
+    set_error("qkv projection: chan must be a positive multiple of 128 (head_dim 128)");
+    return kUnsupported;
+  }
+  if (norm < 0 || norm > 2 || (norm == 2 && !sumsq)) {
+    set_error("qkv projection: norm must be 0, 1 or 2 (2 needs a sumsq workspace)");
+    return kValue;
+  }
+  const int64_t n = 3 * chan;
+  if (out_stride < n || (out_stride * 2) % 16) {
+    set_error("qkv projection: out row stride must be >= 3*chan and 16-byte aligned");
+    return kValue;
+  }
+  if (rows == 0) return kOk;
+  ProjArgs a{};
+  a.out = static_cast<__nv_bfloat16*>(out);
+  a.out_stride = out_stride;
+  a.rows = static_cast<int>(rows);
+  a.chan = static_cast<int>(chan);
+  a.n_cols = static_cast<int>(n);
+  a.n_pairs_m = static_cast<int>((rows + 2 * kPBM - 1) / (2 * kPBM));
+  a.n_tiles_n = static_cast<int>((n + kPBN - 1) / kPBN);
+  a.k_steps = static_cast<int>(chan / kPBK);
+  a.norm = norm;
+  a.gamma_q = gamma_q;
+  a.gamma_k = gamma_k;
+  a.eps = eps;
+  a.sumsq = sumsq;
+  a.rope = reinterpret_cast<const float2*>(rope_table);
+  a.pattern = pattern;
+  a.B = static_cast<int>(batch);
+  a.T = static_cast<int>(t);
+  a.H = static_cast<int>(h);
+  a.W = static_cast<int>(w);
+  a.k = static_cast<int>(k);
+  const int64_t k2 = k * k;
+  a.L = pattern == 0 ? static_cast<int>(t * h * w) : static_cast<int>(t * h * w / k2);
+  a.d_t = (128 - 4 * (128 / 6)) / 2;
+  a.d_h = (2 * (128 / 6)) / 2;
+  if (rope_table) {
+    if (pattern < 0 || pattern > 2 || k < 1 || (pattern == 1 && (h % k || w % k)) ||
+        (pattern == 2 && (h % k2 || w % k2)) || rows % (pattern == 0 ? t * h * w : t * h * w / k2)) {
+      set_error("qkv projection: rope needs a pattern layout consistent with the grid");
+      return kPattern;
+    }
+  }
+  int rc;
+  CUtensorMap ma, mb;
+  if ((rc = make_tmap_bf16_3d(&ma, x, chan, rows, 1, chan, kPBM)) != kOk) return rc;
+  if ((rc = make_tmap_bf16_3d(&mb, w_t, chan, n, 1, chan, kPBN / 2)) != kOk) return rc;
+  static bool attr_set = false;
+  if (!attr_set) {
+    rc = check_cuda(cudaFuncSetAttribute(qkv_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         ProjLayout::kSmem),
+                    "cudaFuncSetAttribute(qkv_gemm)");
+    if (rc != kOk) return rc;
+    attr_set = true;
+  }
+  if (norm == 2) {
+    rc = check_cuda(cudaMemsetAsync(sumsq, 0, rows * 2 * sizeof(float), stream), "memset sumsq");
+    if (rc != kOk) return rc;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int n_units = a.n_pairs_m * a.n_tiles_n;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * min(n_units, sms / 2));
+  cfg.blockDim = dim3(kPThreads);
+  cfg.dynamicSmemBytes = ProjLayout::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  rc = check_cuda(cudaLaunchKernelEx(&cfg, qkv_gemm_kernel, ma, mb, a), "qkv_gemm launch");
+  if (rc != kOk || norm != 2) return rc;
+  const int64_t warps = rows * 2;
+  qk_norm_rope_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, stream>>>(a);
+  return check_cuda(cudaGetLastError(), "qk_norm_rope launch");
+}
+
+}  // namespace osp

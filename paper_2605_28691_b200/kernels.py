@@ -299,3 +299,25 @@ def hif8_decode(codes: torch.Tensor, table: torch.Tensor, dtype=torch.float64,
         codes.data_ptr(), codes.numel(), _lib.ptr(scale), scale_group, table.data_ptr(), out.data_ptr(),
         DTYPE_IDS[dtype], _lib.stream_ptr(codes.device))))
     return out
+
+
+def qkv_project(x: torch.Tensor, w_t: torch.Tensor, norm: int, gamma_q, gamma_k, eps: float,
+                rope_tab, grid, pattern: int, batch: int) -> torch.Tensor:
+    """K6: (rows, C) bf16 @ w_t^T (w_t (3C, C) bf16) with the q/k norm + RoPE epilogue."""
+    L = _lib.lib()
+    _cuda(x, "x")
+    _cuda(w_t, "w_t")
+    if x.dtype != torch.bfloat16 or w_t.dtype != torch.bfloat16:
+        raise UnsupportedError("qkv_project runs bf16 x and weights")
+    rows, C = x.shape
+    if tuple(w_t.shape) != (3 * C, C):
+        raise ShapeError(f"w_t must be (3C, C) = ({3 * C}, {C}), got {tuple(w_t.shape)}")
+    out = torch.empty((rows, 3 * C), dtype=torch.bfloat16, device=x.device)
+    gq = None if gamma_q is None else gamma_q.to(device=x.device, dtype=torch.float32).contiguous()
+    gk = None if gamma_k is None else gamma_k.to(device=x.device, dtype=torch.float32).contiguous()
+    ws = torch.empty((rows, 2), dtype=torch.float32, device=x.device) if norm == 2 else None
+    _lib.check(STATS.run("qkv_project", 2 if norm == 2 else 1, lambda: L.osp_qkv_project(
+        x.data_ptr(), w_t.data_ptr(), out.data_ptr(), rows, C, 3 * C, norm, _lib.ptr(gq), _lib.ptr(gk),
+        float(eps), _lib.ptr(ws), _lib.ptr(rope_tab), grid.t, grid.h, grid.w, grid.k, pattern, batch,
+        _lib.stream_ptr(x.device))))
+    return out
