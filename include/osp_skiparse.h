@@ -182,12 +182,14 @@ int osp_hif8_decode(const uint8_t* codes, int64_t n, const double* scale, int64_
  *           fp32 or NULL (= 1)
  *   rope_table: NULL or (t + h + w, 32) float2 (cos, sin) per axis position and pair; head pairs
  *           (2i, 2i+1) split over (t, h, w) as 22 / 21 / 21 (Wan 3-D RoPE for head_dim 128)
+ *   row_offset: pattern-layout row of x's first row (an SSP shard starts mid-layout)
  * head_dim is 128 (chan % 128 == 0).
  */
 int osp_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, int64_t chan,
                     int64_t out_stride, int norm, const float* gamma_q, const float* gamma_k,
                     float eps, float* sumsq, const float* rope_table, int64_t t, int64_t h,
-                    int64_t w, int64_t k, int pattern, int64_t batch, void* stream);
+                    int64_t w, int64_t k, int pattern, int64_t batch, int64_t row_offset,
+                    void* stream);
 
 /* Self-test of the tcgen05 instruction forms (S = A B^T, O = bf16(S) V for one 128-row tile). */
 int osp_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,

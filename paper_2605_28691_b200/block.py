@@ -48,7 +48,8 @@ def plan_parallel(world: int, k: int) -> tuple[int, int]:
 class SkiparseBlock:
     def __init__(self, g: GridShape, heads: int, chan: int, batch: int = 1, group=None,
                  log: CommLog | None = None, device=None, seeds=(PROJECTION_SEED, PROJECTION_SEED + 1),
-                 transport: str = "native"):
+                 transport: str = "native", qk_norm: str | None = None, rope: bool = False,
+                 eps: float = 1e-6):
         import torch.distributed as dist
         self.g = g
         self.pg: PaddedGrid = pad_grid(g)
@@ -60,6 +61,9 @@ class SkiparseBlock:
         self.rank = dist.get_rank(group) if self.world > 1 else 0
         self.log = log
         self.transport = transport
+        # sec. 8f row 2: QK-RMSNorm ("head" | "channel") and 3-D RoPE fused into the projection
+        # (K6); off = the reference's plain fixed projection (cuBLAS GEMM)
+        self.qk_norm, self.rope, self.eps = qk_norm, rope, eps
         n_sub = g.k * g.k
         if (n_sub * batch) % self.world:
             raise ValueError(f"{n_sub * batch} subsequences do not shard over {self.world} ranks")
@@ -68,6 +72,13 @@ class SkiparseBlock:
         dev = device or torch.device("cuda", torch.cuda.current_device())
         self.W1 = packed_projection(chan, COMPUTE_DTYPE, dev, seeds[0])
         self.W2 = packed_projection(chan, COMPUTE_DTYPE, dev, seeds[1])
+        self.prologue = qk_norm is not None or rope
+        if self.prologue:
+            from .prologue import packed_projection_t
+            self.W1t = packed_projection_t(chan, dev, seeds[0])
+            self.W2t = packed_projection_t(chan, dev, seeds[1])
+            self.gamma_q = torch.ones(chan, device=dev)
+            self.gamma_k = torch.ones(chan, device=dev)
         r0, r1 = self.rank * self.local_rows, (self.rank + 1) * self.local_rows
         bt = self.pg.mask_bits(SparsePattern.TOKEN_WISE, batch)
         bg = self.pg.mask_bits(SparsePattern.GROUP_WISE, batch)
@@ -87,15 +98,22 @@ class SkiparseBlock:
             return self._g2t.apply(x)
         return ssp_switch(x, self.grid, self.group, self.log, self.transport)
 
-    def attend(self, x, W, bits):
-        qkv = torch.matmul(x, W)
+    def attend(self, x, W, bits, pattern=SparsePattern.TOKEN_WISE):
+        if self.prologue:
+            from .prologue import QKVPrologue
+            Wt = self.W1t if W is self.W1 else self.W2t
+            qkv = QKVPrologue.apply(x, self.grid, pattern, self.batch, self.qk_norm, self.gamma_q,
+                                    self.gamma_k, self.eps, self.rope,
+                                    self.rank * self.local_rows * self.L, Wt)
+        else:
+            qkv = torch.matmul(x, W)
         return attention_packed(qkv, self.heads, bits, zero_invalid_queries=bits is not None)
 
     def __call__(self, x_tsa: torch.Tensor) -> torch.Tensor:
         """x_tsa: this rank's (G*B, L, C) bf16 shard in the token-wise layout."""
         o1 = self.attend(x_tsa, self.W1, self.bits_tsa)
         x2 = self.switch_to_gsa(o1)
-        o2 = self.attend(x2, self.W2, self.bits_gsa)
+        o2 = self.attend(x2, self.W2, self.bits_gsa, SparsePattern.GROUP_WISE)
         return self.switch_to_tsa(o2)
 
     # ------------------------------------------------------------------ layouts

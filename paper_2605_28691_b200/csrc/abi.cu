@@ -395,13 +395,14 @@ int osp_hif8_decode(const uint8_t* codes, int64_t n, const double* scale, int64_
 int osp_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, int64_t chan,
                     int64_t out_stride, int norm, const float* gamma_q, const float* gamma_k,
                     float eps, float* sumsq, const float* rope_table, int64_t t, int64_t h,
-                    int64_t w, int64_t k, int pattern, int64_t batch, void* stream) {
+                    int64_t w, int64_t k, int pattern, int64_t batch, int64_t row_offset,
+                    void* stream) {
   if (rows < 0 || chan <= 0 || !x || !w_t || !out) {
     set_error("qkv projection: bad sizes or null pointers");
     return kValue;
   }
   return launch_qkv_project(x, w_t, out, rows, chan, out_stride, norm, gamma_q, gamma_k, eps, sumsq,
-                            rope_table, t, h, w, k, pattern, batch, as_stream(stream));
+                            rope_table, t, h, w, k, pattern, batch, row_offset, as_stream(stream));
 }
 
 int osp_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,

@@ -52,11 +52,13 @@ struct ProjArgs {
   const float2* rope;       // (T + H + W, 32) cos/sin, or null
   int pattern;              // 0 original, 1 TSA, 2 GSA
   int B, T, H, W, k, L;     // padded grid, batch, subsequence length
+  int row_offset;           // global pattern-layout row of local row 0 (SSP shards)
   int d_t, d_h;             // pairs on the t and h axes (the rest on w)
 };
 
 // Padded-grid (t, h, w) of pattern-layout row `r` (inverse of skiparse.py:68-114).
 __device__ __forceinline__ void row_coords(const ProjArgs& a, int r, int& t, int& h, int& w) {
+  r += a.row_offset;
   if (a.pattern == 0) {
     const int pos = r % (a.T * a.H * a.W);
     w = pos % a.W;
@@ -314,7 +316,8 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(ProjArgs a) {
 int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, int64_t chan,
                        int64_t out_stride, int norm, const float* gamma_q, const float* gamma_k,
                        float eps, float* sumsq, const float* rope_table, int64_t t, int64_t h,
-                       int64_t w, int64_t k, int pattern, int64_t batch, cudaStream_t stream) {
+                       int64_t w, int64_t k, int pattern, int64_t batch, int64_t row_offset,
+                       cudaStream_t stream) {
   if (chan % 128 != 0 || chan < 128) {
     set_error("qkv projection: chan must be a positive multiple of 128 (head_dim 128)");
     return kUnsupported;
@@ -350,13 +353,15 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   a.H = static_cast<int>(h);
   a.W = static_cast<int>(w);
   a.k = static_cast<int>(k);
+  a.row_offset = static_cast<int>(row_offset);
   const int64_t k2 = k * k;
   a.L = pattern == 0 ? static_cast<int>(t * h * w) : static_cast<int>(t * h * w / k2);
   a.d_t = (128 - 4 * (128 / 6)) / 2;
   a.d_h = (2 * (128 / 6)) / 2;
   if (rope_table) {
     if (pattern < 0 || pattern > 2 || k < 1 || (pattern == 1 && (h % k || w % k)) ||
-        (pattern == 2 && (h % k2 || w % k2)) || rows % (pattern == 0 ? t * h * w : t * h * w / k2)) {
+        (pattern == 2 && (h % k2 || w % k2)) || row_offset < 0 ||
+        (rows + row_offset) > (pattern == 0 ? batch * t * h * w : batch * t * h * w)) {
       set_error("qkv projection: rope needs a pattern layout consistent with the grid");
       return kPattern;
     }

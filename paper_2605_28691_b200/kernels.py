@@ -302,7 +302,7 @@ def hif8_decode(codes: torch.Tensor, table: torch.Tensor, dtype=torch.float64,
 
 
 def qkv_project(x: torch.Tensor, w_t: torch.Tensor, norm: int, gamma_q, gamma_k, eps: float,
-                rope_tab, grid, pattern: int, batch: int) -> torch.Tensor:
+                rope_tab, grid, pattern: int, batch: int, row_offset: int = 0) -> torch.Tensor:
     """K6: (rows, C) bf16 @ w_t^T (w_t (3C, C) bf16) with the q/k norm + RoPE epilogue."""
     L = _lib.lib()
     _cuda(x, "x")
@@ -319,5 +319,5 @@ def qkv_project(x: torch.Tensor, w_t: torch.Tensor, norm: int, gamma_q, gamma_k,
     _lib.check(STATS.run("qkv_project", 2 if norm == 2 else 1, lambda: L.osp_qkv_project(
         x.data_ptr(), w_t.data_ptr(), out.data_ptr(), rows, C, 3 * C, norm, _lib.ptr(gq), _lib.ptr(gk),
         float(eps), _lib.ptr(ws), _lib.ptr(rope_tab), grid.t, grid.h, grid.w, grid.k, pattern, batch,
-        _lib.stream_ptr(x.device))))
+        row_offset, _lib.stream_ptr(x.device))))
     return out

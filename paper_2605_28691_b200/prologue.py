@@ -20,7 +20,7 @@ from .attention import PROJECTION_SEED, qkv_projections
 from .gridseq import GridShape, default_device
 from .skiparse import SparsePattern
 
-__all__ = ["rope_table", "packed_projection_t", "qkv_project", "ROPE_THETA"]
+__all__ = ["rope_table", "packed_projection_t", "qkv_project", "QKVPrologue", "ROPE_THETA"]
 
 ROPE_THETA = 10000.0
 _PATTERN_IDS = {SparsePattern.ORIGINAL: 0, SparsePattern.TOKEN_WISE: 1, SparsePattern.GROUP_WISE: 2}
@@ -65,7 +65,8 @@ def packed_projection_t(chan: int, device=None, seed: int = PROJECTION_SEED) -> 
 def qkv_project(x: torch.Tensor, grid: GridShape, pattern: SparsePattern = SparsePattern.ORIGINAL,
                 batch: int = 1, norm: str | None = None, gamma_q: torch.Tensor | None = None,
                 gamma_k: torch.Tensor | None = None, eps: float = 1e-6, rope: bool = False,
-                weight_t: torch.Tensor | None = None, theta: float = ROPE_THETA) -> torch.Tensor:
+                weight_t: torch.Tensor | None = None, theta: float = ROPE_THETA,
+                row_offset: int = 0) -> torch.Tensor:
     """x: (rows, L, C) or (rows*L, C) bf16 in `pattern` layout on the padded `grid` with `batch`
     items.  Returns q | k | v as (..., 3C) bf16.  head_dim is 128 (C % 128 == 0)."""
     if norm not in _NORMS:
@@ -79,5 +80,72 @@ def qkv_project(x: torch.Tensor, grid: GridShape, pattern: SparsePattern = Spars
     w_t = weight_t if weight_t is not None else packed_projection_t(C, x2.device)
     out = kernels.qkv_project(x2, w_t, _NORMS[norm], gamma_q, gamma_k, eps,
                               rope_table(grid, 128, theta, x2.device) if rope else None,
-                              grid, _PATTERN_IDS[SparsePattern(pattern)], batch)
+                              grid, _PATTERN_IDS[SparsePattern(pattern)], batch, row_offset)
     return out.view(*shape[:-1], 3 * C)
+
+
+def _rope_cos_sin(grid: GridShape, pattern, batch: int, rows: int, row_offset: int, device, theta):
+    """(rows, 64) cos / sin of every pair's angle (backward only)."""
+    from .skiparse import assignment_of
+    pat = SparsePattern(pattern)
+    if pat is SparsePattern.ORIGINAL:
+        flat = torch.arange(grid.seq_len, device=device)
+        src = flat.repeat(batch)
+    else:
+        from .skiparse import pattern_map
+        src = pattern_map(grid, pat, batch).src.reshape(-1) % grid.seq_len
+    src = src[row_offset:row_offset + rows]
+    t, h, w = src // (grid.h * grid.w), (src // grid.w) % grid.h, src % grid.w
+    tab = rope_table(grid, 128, theta, device)                      # (t+h+w, 32, 2)
+    dt, dh, dw = (d // 2 for d in rope_axes(128))
+    cs = torch.cat([tab[t, :dt], tab[grid.t + h, :dh], tab[grid.t + grid.h + w, :dw]], dim=1)
+    return cs[..., 0], cs[..., 1]
+
+
+class QKVPrologue(torch.autograd.Function):
+    """K6 forward; backward = inverse RoPE rotation, RMSNorm backward (fp32 torch on the
+    device), then dx = d(pre-norm qkv) @ W^T.  Weights and gammas are fixed (no grad), like the
+    reference's seeded projections."""
+
+    @staticmethod
+    def forward(ctx, x, grid, pattern, batch, norm, gamma_q, gamma_k, eps, rope, row_offset,
+                weight_t=None):
+        C = x.shape[-1]
+        w_t = weight_t if weight_t is not None else packed_projection_t(C, x.device)
+        out = qkv_project(x, grid, pattern, batch, norm, gamma_q, gamma_k, eps, rope,
+                          weight_t=w_t, row_offset=row_offset)
+        ctx.save_for_backward(x)
+        ctx.cfg = (grid, pattern, batch, norm, gamma_q, gamma_k, eps, rope, row_offset, C, w_t)
+        return out
+
+    @staticmethod
+    def backward(ctx, gout):
+        (x,) = ctx.saved_tensors
+        grid, pattern, batch, norm, gamma_q, gamma_k, eps, rope, row_offset, C, w_t = ctx.cfg
+        shape = x.shape
+        rows = x.numel() // C
+        g = gout.reshape(rows, 3 * C).float()
+        if norm is not None or rope:
+            y = qkv_project(x, grid, pattern, batch, weight_t=w_t).reshape(rows, 3 * C).float() if norm else None
+            if rope:
+                c, s = _rope_cos_sin(grid, pattern, batch, rows, row_offset, x.device, ROPE_THETA)
+            parts = []
+            for which, gamma in ((0, gamma_q), (1, gamma_k)):
+                d = g[:, which * C:(which + 1) * C]
+                if rope:   # transpose of the pair rotation
+                    d2 = d.view(rows, -1, 64, 2)
+                    d0, d1 = d2[..., 0], d2[..., 1]
+                    d = torch.stack([d0 * c[:, None] + d1 * s[:, None],
+                                     -d0 * s[:, None] + d1 * c[:, None]], dim=-1).reshape(rows, C)
+                if norm is not None:
+                    yy = y[:, which * C:(which + 1) * C]
+                    n = C if norm == "channel" else 128
+                    yg = yy.view(rows, -1, n)
+                    dg = (d * (gamma.float() if gamma is not None else 1.0)).view(rows, -1, n)
+                    r = torch.rsqrt((yg * yg).mean(-1, keepdim=True) + eps)
+                    d = (r * dg - yg * (r ** 3) * (dg * yg).mean(-1, keepdim=True)).reshape(rows, C)
+                parts.append(d)
+            parts.append(g[:, 2 * C:])
+            g = torch.cat(parts, dim=1)
+        dx = (g.to(torch.bfloat16) @ w_t).reshape(shape)
+        return dx, None, None, None, None, None, None, None, None, None, None

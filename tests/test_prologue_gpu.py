@@ -78,3 +78,57 @@ def test_prologue_errors(P):
         qkv_project(torch.zeros(64, 96, device="cuda", dtype=torch.bfloat16), g)
     with pytest.raises(ValueError):
         qkv_project(torch.zeros(64, 128, device="cuda", dtype=torch.bfloat16), g, norm="layer")
+
+
+@pytest.mark.parametrize("norm,rope", [(None, True), ("head", True), ("channel", True), ("head", False)])
+def test_prologue_backward_matches_float64_autograd(P, norm, rope):
+    """QKVPrologue backward (inverse RoPE, RMSNorm backward, dx = dqkv W^T) vs float64 autograd
+    of the reference prologue."""
+    from paper_2605_28691_b200.prologue import QKVPrologue, packed_projection_t
+    g = P.GridShape(2, 8, 8, 2)
+    og = O.Grid(2, 8, 8, 2)
+    C = 256
+    torch.manual_seed(1)
+    x = torch.randn(4, g.seq_len // 4, C, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    gq = torch.rand(C, device="cuda") + 0.5
+    gk = torch.rand(C, device="cuda") + 0.5
+    w_t = packed_projection_t(C, "cuda")
+    y = QKVPrologue.apply(x, g, P.SparsePattern.TOKEN_WISE, 1, norm, gq, gk, 1e-6, rope, 0, w_t)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    xr = x.detach().double().cpu().reshape(-1, C).requires_grad_(True)
+    pos = R.pattern_positions(og, "tsa", 1)
+    ref = R.qkv_prologue_ref(xr, w_t.t().double().cpu(), pos, norm, gq.cpu(), gk.cpu(), rope=rope)
+    ref.backward(gy.double().cpu().reshape(-1, 3 * C))
+    got = x.grad.double().cpu().reshape(-1, C)
+    err = (got - xr.grad).abs().max().item()
+    assert err <= 2e-2 * xr.grad.abs().max().item(), err
+
+
+def test_block_with_prologue_matches_float64_composition(P):
+    """SkiparseBlock with QK-RMSNorm + RoPE equals the float64 composition: prologue_ref ->
+    attention per subsequence -> TSA->GSA switch (oracle table) -> prologue_ref -> attention ->
+    GSA->TSA switch."""
+    from paper_2605_28691_b200.block import SkiparseBlock
+    grid = (2, 8, 8, 2)
+    g = P.GridShape(*grid)
+    og = O.Grid(*grid)
+    C, heads = 256, 2
+    blk = SkiparseBlock(g, heads, C, qk_norm="head", rope=True)
+    torch.manual_seed(2)
+    x = torch.randn(blk.local_rows, blk.L, C, device="cuda").to(torch.bfloat16)
+    y = blk(x).double().cpu()
+
+    def app(xl, w_t, pattern):
+        pos = R.pattern_positions(og, pattern, 1)
+        qkv = R.qkv_prologue_ref(xl.reshape(-1, C), w_t.t().double().cpu(), pos, "head", None, None,
+                                 rope=True).reshape(4, -1, 3 * C)
+        return R.attention_ref(qkv[..., :C], qkv[..., C:2 * C], qkv[..., 2 * C:], heads)
+
+    xd = x.double().cpu()
+    o1 = app(xd, blk.W1t, "tsa")
+    x2 = torch.from_numpy(O.apply_table(O.map_table("tsa_to_gsa", og, 1), o1.numpy()))
+    o2 = app(x2, blk.W2t, "gsa")
+    want = torch.from_numpy(O.apply_table(O.map_table("gsa_to_tsa", og, 1), o2.numpy()))
+    err = (y - want).abs().max().item()
+    assert err < 3e-2, err
