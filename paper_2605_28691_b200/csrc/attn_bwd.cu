@@ -492,7 +492,9 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
                  tDK = tmem + 384;
   const int64_t sh = static_cast<int64_t>(seq) * a.heads + head;
 
+  // register budget (setmaxnreg, total < 64K): control warps 56, compute 176, writers 88
   if (warp < 4) {
+    regs_dec<56>();
     if (warp == 0) {
       if (elect_one()) {
       // ---------------------------------------------------------------- TMA producer
@@ -615,6 +617,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       __syncwarp();
     }
   } else if (warp < 12) {
+    regs_inc<176>();
     // ------------------------------------------------------------------ compute warps: thread =
     // key row, the two warpgroups split the 64 query columns of a tile (32 each)
     const int half = (warp - 4) >> 2;
@@ -640,6 +643,22 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       const float* lse_s = reinterpret_cast<const float*>(sm + Ly::kStat + st * 512) + half * 32;
       const float* del_s = lse_s + 64;
       mbar_wait(bar_qf + st, (i / 3) & 1);
+      // lse2 / delta of this tile's 32 query columns into registers now: shared memory is busy
+      // feeding SS-mode MMAs, so these loads must not sit on the softmax critical path
+      float lse_r[32], del_r[32];
+#pragma unroll
+      for (int j4 = 0; j4 < 8; ++j4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(lse_s + j4 * 4);
+        const float4 d4 = *reinterpret_cast<const float4*>(del_s + j4 * 4);
+        lse_r[j4 * 4 + 0] = l4.x;
+        lse_r[j4 * 4 + 1] = l4.y;
+        lse_r[j4 * 4 + 2] = l4.z;
+        lse_r[j4 * 4 + 3] = l4.w;
+        del_r[j4 * 4 + 0] = d4.x;
+        del_r[j4 * 4 + 1] = d4.y;
+        del_r[j4 * 4 + 2] = d4.z;
+        del_r[j4 * 4 + 3] = d4.w;
+      }
       mbar_wait(bar_s, i & 1);
       tc_fence_after();
       if (a.flags & 2) {  // experiment: synchronisation skeleton only
@@ -658,13 +677,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         tmem_ld32(tS + la + half * 32, s0);
         tmem_wait_ld(s0);
 #pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          const float4 l0 = *reinterpret_cast<const float4*>(lse_s + j4 * 4);
-          p[j4 * 4 + 0] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 0]), c, -l0.x));
-          p[j4 * 4 + 1] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 1]), c, -l0.y));
-          p[j4 * 4 + 2] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 2]), c, -l0.z));
-          p[j4 * 4 + 3] = ex2(fmaf(__uint_as_float(s0[j4 * 4 + 3]), c, -l0.w));
-        }
+        for (int j = 0; j < 32; ++j) p[j] = ex2(fmaf(__uint_as_float(s0[j]), c, -lse_r[j]));
       }
       if (!kvalid) {
 #pragma unroll
@@ -691,9 +704,8 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float2 d2 = *reinterpret_cast<const float2*>(del_s + 2 * j);
-          const float ds0 = p[2 * j] * (__uint_as_float(dp[2 * j]) - d2.x);
-          const float ds1 = p[2 * j + 1] * (__uint_as_float(dp[2 * j + 1]) - d2.y);
+          const float ds0 = p[2 * j] * (__uint_as_float(dp[2 * j]) - del_r[2 * j]);
+          const float ds1 = p[2 * j + 1] * (__uint_as_float(dp[2 * j + 1]) - del_r[2 * j + 1]);
           pk[j] = pack_bf16(ds0, ds1);
         }
 #pragma unroll
@@ -742,6 +754,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       }
     }
   } else {
+    regs_dec<88>();
     // ------------------------------------------------------------------ dQ^T writer warps (thread = d)
     const int wq = warp & 3;
     const uint32_t la = static_cast<uint32_t>(wq * 32) << 16;
