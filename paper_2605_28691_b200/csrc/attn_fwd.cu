@@ -52,7 +52,8 @@ struct FwdArgs {
   int n_kv;
   float scale_log2;
   int zero_invalid_q;
-  int flags;  // debug experiments (OSP_FWD_FLAGS): 1 = no exp, 2 = softmax skeleton only
+  int flags;  // debug experiments (OSP_FWD_FLAGS): 1 = no exp, 2 = softmax skeleton only,
+             // 4 = no exp-phase ping-pong
 };
 
 __device__ __forceinline__ bool bit_at(const uint32_t* bits, int words, int i) {
@@ -219,7 +220,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // finishes within the window the other tile's MMAs cover, instead of both running at half
     // speed.  Warpgroup 1 opens the first turn for warpgroup 0.
     const uint32_t my_turn = 2 + t, next_turn = 3 - t;
-    if (t == 1) asm volatile("bar.arrive %0, 256;" ::"r"(2u) : "memory");
+    const bool pingpong = !(a.flags & 4);  // experiment 4: no exp-phase serialisation
+    if (t == 1 && pingpong) asm volatile("bar.arrive %0, 256;" ::"r"(2u) : "memory");
 
     float m_used = -INFINITY;
     float l = 0.f;
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             ls1 += p1;
             pk[i] = pack_bf16(p0, p1);
           }
-          if (turn && cc == 3 && !(t == 1 && j == a.n_kv - 1))
+          if (turn && pingpong && cc == 3 && !(t == 1 && j == a.n_kv - 1))
             asm volatile("bar.arrive %0, 256;" ::"r"(next_turn) : "memory");
           tmem_st16(tS + cc * 16, pk);
         }
@@ -326,14 +328,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         // no running max yet: exact row max first
         const float m_new = fmaxf(m_used, row_max());
         if (__any_sync(0xFFFFFFFFu, needs_rescale(m_new))) rescale(m_new);
-        named_bar_sync(my_turn, 256);
+        if (pingpong) named_bar_sync(my_turn, 256);
         exps(true);
       } else {
         // Speculative: exponentiate against the running max straight away (values up to 2^8
         // above it are fine for bf16 P and the fp32 sums -- the lazy-rescale threshold) while
         // the row max is reduced off the MUFU critical path; a tile that overshoots by more is
         // rescaled and redone (rare once the max has settled).
-        named_bar_sync(my_turn, 256);
+        if (pingpong) named_bar_sync(my_turn, 256);
         exps(true);
         const float m_new = fmaxf(m_used, row_max());
         if (__any_sync(0xFFFFFFFFu, needs_rescale(m_new))) {
