@@ -108,17 +108,21 @@ int osp_mask_bits_to_bytes(const uint32_t* bits, uint8_t* valid, int64_t n_rows,
  *             no valid key or (zero_invalid_queries) an invalid query.
  *   valid_bits: NULL or (n_seq, ceil(seq_len/32)) key validity (attention.py:35-44 rules:
  *             masked keys weigh 0, an all-masked row outputs 0).
+ *   seq_lens: NULL or (n_seq) int32 per-sequence lengths <= seq_len: sequence s uses only its
+ *             first seq_lens[s] rows as queries and keys (rows beyond are not read as keys and
+ *             not written).  This runs subsequences with their padding compacted away.
  *   zero_invalid_queries: rows whose own bit is 0 output 0 (attention.py:127-130).
  *   scale   : softmax scale (reference: 1/sqrt(chan) with one head, attention.py:57).
  */
 int osp_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n_seq,
                  int64_t seq_len, int64_t heads, int64_t head_dim, int64_t q_stride,
                  int64_t k_stride, int64_t v_stride, int64_t o_stride, const uint32_t* valid_bits,
-                 int zero_invalid_queries, float scale, void* stream);
+                 const int32_t* seq_lens, int zero_invalid_queries, float scale, void* stream);
 
 /*
  * K3: backward of osp_attn_fwd (no reference counterpart: attention.py has no backward).
- * Writes dq, dk, dv (bf16, own row strides).  workspace >= osp_attn_bwd_workspace_bytes().
+ * Writes dq, dk, dv (bf16, own row strides; with seq_lens, rows beyond a sequence's length get
+ * dq = 0 and dk, dv untouched).  workspace >= osp_attn_bwd_workspace_bytes().
  */
 size_t osp_attn_bwd_workspace_bytes(int64_t n_seq, int64_t seq_len, int64_t heads,
                                     int64_t head_dim);
@@ -127,8 +131,8 @@ int osp_attn_bwd(const void* q, const void* k, const void* v, const void* o, con
                  int64_t heads, int64_t head_dim, int64_t q_stride, int64_t k_stride,
                  int64_t v_stride, int64_t o_stride, int64_t do_stride, int64_t dq_stride,
                  int64_t dk_stride, int64_t dv_stride, const uint32_t* valid_bits,
-                 int zero_invalid_queries, float scale, void* workspace, size_t workspace_bytes,
-                 void* stream);
+                 const int32_t* seq_lens, int zero_invalid_queries, float scale, void* workspace,
+                 size_t workspace_bytes, void* stream);
 
 /*
  * K4: Sparse Sequence Parallel pattern switch, local steps of ssp_pattern_switch

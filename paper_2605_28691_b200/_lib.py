@@ -34,11 +34,11 @@ _SIGS = {
     "osp_mask_bytes_to_bits": ([c_vp, c_vp, c_i64, c_i64, c_vp], c_int),
     "osp_mask_bits_to_bytes": ([c_vp, c_vp, c_i64, c_i64, c_vp], c_int),
     "osp_attn_fwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
-                      c_i64, c_vp, c_int, c_f, c_vp], c_int),
+                      c_i64, c_vp, c_vp, c_int, c_f, c_vp], c_int),
     "osp_attn_bwd_workspace_bytes": ([c_i64, c_i64, c_i64, c_i64], ctypes.c_size_t),
     "osp_attn_bwd": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64,
-                      c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_int,
-                      c_f, c_vp, ctypes.c_size_t, c_vp], c_int),
+                      c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp,
+                      c_int, c_f, c_vp, ctypes.c_size_t, c_vp], c_int),
     "osp_ssp_pack": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp],
                      c_int),
     "osp_ssp_unpack": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp],

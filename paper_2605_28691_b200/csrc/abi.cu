@@ -262,14 +262,14 @@ static int attn_checks(int64_t n_seq, int64_t seq_len, int64_t heads, int64_t he
 int osp_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n_seq,
                  int64_t seq_len, int64_t heads, int64_t head_dim, int64_t q_stride,
                  int64_t k_stride, int64_t v_stride, int64_t o_stride, const uint32_t* valid_bits,
-                 int zero_invalid_queries, float scale, void* stream) {
+                 const int32_t* seq_lens, int zero_invalid_queries, float scale, void* stream) {
   int rc = attn_checks(n_seq, seq_len, heads, head_dim);
   if (rc != kOk) return rc;
   if ((o_stride * 2) % 16 || (reinterpret_cast<uintptr_t>(o) & 15)) {
     set_error("output needs 16-byte aligned base and row stride");
     return kValue;
   }
-  AttnShape s{n_seq, seq_len, heads, head_dim};
+  AttnShape s{n_seq, seq_len, heads, head_dim, seq_lens};
   return launch_attn_fwd(q, k, v, o, lse, s, q_stride, k_stride, v_stride, o_stride, valid_bits,
                          zero_invalid_queries, scale, as_stream(stream));
 }
@@ -285,11 +285,11 @@ int osp_attn_bwd(const void* q, const void* k, const void* v, const void* o, con
                  int64_t heads, int64_t head_dim, int64_t q_stride, int64_t k_stride,
                  int64_t v_stride, int64_t o_stride, int64_t do_stride, int64_t dq_stride,
                  int64_t dk_stride, int64_t dv_stride, const uint32_t* valid_bits,
-                 int zero_invalid_queries, float scale, void* workspace, size_t workspace_bytes,
-                 void* stream) {
+                 const int32_t* seq_lens, int zero_invalid_queries, float scale, void* workspace,
+                 size_t workspace_bytes, void* stream) {
   int rc = attn_checks(n_seq, seq_len, heads, head_dim);
   if (rc != kOk) return rc;
-  AttnShape s{n_seq, seq_len, heads, head_dim};
+  AttnShape s{n_seq, seq_len, heads, head_dim, seq_lens};
   if (workspace_bytes < attn_bwd_workspace_bytes(s)) {
     set_error("attention backward workspace too small");
     return kValue;

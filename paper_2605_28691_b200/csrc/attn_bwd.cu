@@ -49,7 +49,8 @@ struct BwdArgs {
   int64_t dk_stride, dv_stride;
   const uint32_t* valid_bits;
   int words_per_seq;
-  int seq_len, seq_pad, heads, n_q;
+  int seq_len, seq_pad, heads, n_q;  // seq_len = capacity (row stride of a sequence)
+  const int* seq_lens;               // per-sequence valid length (<= seq_len) or null
   float scale, scale_log2;
   const __nv_bfloat16* k_rows;  // K (for the TMEM copy of the key tile)
   int64_t k_row_stride;
@@ -121,6 +122,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int head = blockIdx.y;
   const int seq = blockIdx.z;
   const int kv0 = blockIdx.x * 128;
+  const int len = a.seq_lens ? __ldg(a.seq_lens + seq) : a.seq_len;
+  if (kv0 >= len) return;
+  const int n_q = (len + 127) / 128;
 
   if ((smem_u32(sm) & 1023) != 0) __trap();
 
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_load_3d(sm + Ly::kK + s * 16384, &tmK, bar_kv, head * D + s * 64, kv0, seq);
         tma_load_3d(sm + Ly::kV + s * 16384, &tmV, bar_kv, head * D + s * 64, kv0, seq);
       }
-      for (int i = 0; i < a.n_q; ++i) {
+      for (int i = 0; i < n_q; ++i) {
         const int st = i & 1;
         mbar_wait(bar_qe + st, ((i >> 1) & 1) ^ 1);
         mbar_expect_tx(bar_qf + st, 2 * Ly::kTile + 1024);
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint32_t v_base = smem_u32(sm + Ly::kV);
       const uint32_t ds_base = smem_u32(sm + Ly::kDS);
       mbar_wait(bar_kv, 0);
-      for (int i = 0; i < a.n_q; ++i) {
+      for (int i = 0; i < n_q; ++i) {
         const int st = i & 1;
         const uint32_t q_base = smem_u32(sm + Ly::kQ + st * Ly::kTile);
         const uint32_t do_base = smem_u32(sm + Ly::kDO + st * Ly::kTile);
@@ -254,14 +258,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
     const int krow = wq * 32 + lane;  // key row within the tile
     const int kglob = kv0 + krow;
-    bool kvalid = kglob < a.seq_len;
+    bool kvalid = kglob < len;
     if (kvalid && a.valid_bits) {
       const uint32_t* vb = a.valid_bits + static_cast<int64_t>(seq) * a.words_per_seq;
       kvalid = (__ldg(vb + (kglob >> 5)) >> (kglob & 31)) & 1u;
     }
     const float c = a.scale_log2;
     uint8_t* ds_row0 = sm + Ly::kDS + krow * 128;
-    for (int i = 0; i < a.n_q; ++i) {
+    for (int i = 0; i < n_q; ++i) {
       const int st = i & 1;
       const float* lse_s = reinterpret_cast<const float*>(sm + Ly::kStat + st * 1024);
       const float* del_s = lse_s + 128;
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ---------------------------------------------------------------- dK / dV epilogue
     mbar_wait(bar_fin, 0);
     tc_fence_after();
-    const bool row_ok = kglob < a.seq_len;
+    const bool row_ok = kglob < len;
     __nv_bfloat16* dvrow = a.dv + (static_cast<int64_t>(seq) * a.seq_len + kglob) * a.dv_stride +
                            static_cast<int64_t>(head) * D;
     __nv_bfloat16* dkrow = a.dk + (static_cast<int64_t>(seq) * a.seq_len + kglob) * a.dk_stride +
@@ -368,7 +372,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int wq = warp & 3;
     const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
     const int qrow = wq * 32 + lane;
-    for (int i = 0; i < a.n_q; ++i) {
+    for (int i = 0; i < n_q; ++i) {
       mbar_wait(bar_dq, i & 1);
       tc_fence_after();
       const int qg = i * 128 + qrow;
@@ -382,7 +386,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tc_fence_before();
           mbar_arrive(bar_dqf);
         }
-        if (qg < a.seq_len && !(a.flags & 1)) {
+        if (qg < len && !(a.flags & 1)) {
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             red_add_v4(dst + cc * 32 + j * 4, __uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
@@ -458,7 +462,9 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
   const int head = blockIdx.y;
   const int seq = blockIdx.z;
   const int kv0 = blockIdx.x * 128;
-  const int n_q = (a.seq_len + 63) / 64;
+  const int len = a.seq_lens ? __ldg(a.seq_lens + seq) : a.seq_len;
+  if (kv0 >= len) return;
+  const int n_q = (len + 63) / 64;
 
   if ((smem_u32(sm) & 1023) != 0) __trap();
   if (threadIdx.x == 0) {
@@ -625,14 +631,14 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
     const uint32_t la = static_cast<uint32_t>(wq * 32) << 16;
     const int krow = wq * 32 + lane;
     const int kglob = kv0 + krow;
-    bool kvalid = kglob < a.seq_len;
+    bool kvalid = kglob < len;
     if (kvalid && a.valid_bits) {
       const uint32_t* vb = a.valid_bits + static_cast<int64_t>(seq) * a.words_per_seq;
       kvalid = (__ldg(vb + (kglob >> 5)) >> (kglob & 31)) & 1u;
     }
     if (half == 0)
       row_to_tmem(tK + la, a.k_rows + (static_cast<int64_t>(seq) * a.seq_len + kglob) * a.k_row_stride +
-                               static_cast<int64_t>(head) * D, kglob < a.seq_len);
+                               static_cast<int64_t>(head) * D, kglob < len);
     tmem_wait_st();
     tc_fence_before();
     mbar_arrive(bar_kt);
@@ -727,7 +733,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
     // (warpgroup 0 drains dV, warpgroup 1 drains dK)
     mbar_wait(bar_fin, 0);
     tc_fence_after();
-    const bool row_ok = kglob < a.seq_len;
+    const bool row_ok = kglob < len;
     {
       const int which = half;
       const uint32_t base = (which == 0 ? tDV : tDK) + la;
@@ -818,7 +824,7 @@ template <int D>
 __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t o_stride,
                                 const __nv_bfloat16* __restrict__ dout, int64_t do_stride,
                                 const float* __restrict__ lse, float* lse2, float* delta, int64_t n_seq,
-                                int heads, int seq_len, int seq_pad) {
+                                int heads, int seq_len, int seq_pad, const int* __restrict__ seq_lens) {
   const int64_t total = n_seq * heads * static_cast<int64_t>(seq_pad);
   const int lane = threadIdx.x & 31;
   for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total;
@@ -827,8 +833,9 @@ __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t o_s
     const int64_t sh = w / seq_pad;
     const int h = static_cast<int>(sh % heads);
     const int64_t s = sh / heads;
+    const int len = seq_lens ? __ldg(seq_lens + s) : seq_len;
     float acc = 0.f;
-    if (q < seq_len) {
+    if (q < len) {
       const __nv_bfloat16* orow = o + (s * seq_len + q) * o_stride + static_cast<int64_t>(h) * D;
       const __nv_bfloat16* drow = dout + (s * seq_len + q) * do_stride + static_cast<int64_t>(h) * D;
       for (int c = lane * 2; c < D; c += 64) {
@@ -841,7 +848,7 @@ __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t o_s
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, off);
     if (lane == 0) {
       delta[w] = acc;
-      lse2[w] = q < seq_len ? lse[sh * seq_len + q] * kLog2e : INFINITY;
+      lse2[w] = q < len ? lse[sh * seq_len + q] * kLog2e : INFINITY;
     }
   }
 }
@@ -902,7 +909,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     bwd_prep_kernel<D><<<grid_for(rows * 32, 256), 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(o), os, static_cast<const __nv_bfloat16*>(dout), dos, lse,
         w.lse2, w.delta, s.n_seq, static_cast<int>(s.heads), static_cast<int>(s.seq_len),
-        static_cast<int>(seq_pad));
+        static_cast<int>(seq_pad), s.seq_lens);
     rc = check_cuda(cudaGetLastError(), "bwd_prep launch");
     if (rc != kOk) return rc;
   }
@@ -929,6 +936,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
   a.valid_bits = bits;
   a.words_per_seq = static_cast<int>((s.seq_len + 31) / 32);
   a.seq_len = static_cast<int>(s.seq_len);
+  a.seq_lens = s.seq_lens;
   a.seq_pad = static_cast<int>(seq_pad);
   a.heads = static_cast<int>(s.heads);
   a.n_q = static_cast<int>(seq_pad / 128);

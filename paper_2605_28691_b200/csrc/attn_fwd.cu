@@ -47,9 +47,9 @@ struct FwdArgs {
   float* lse;
   const uint32_t* valid_bits;
   int words_per_seq;
-  int seq_len;
+  int seq_len;              // capacity (row stride of a sequence)
+  const int* seq_lens;      // per-sequence valid length (<= seq_len) or null
   int heads;
-  int n_kv;
   float scale_log2;
   int zero_invalid_q;
   int flags;  // debug experiments (OSP_FWD_FLAGS): 1 = no exp, 2 = softmax skeleton only,
@@ -85,6 +85,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int head = blockIdx.y;
   const int seq = blockIdx.z;
   const int q_row0 = blockIdx.x * 2 * kBM;
+  // variable-length sequences: rows >= len are neither keys nor queries (compacted layouts)
+  const int len = a.seq_lens ? __ldg(a.seq_lens + seq) : a.seq_len;
+  if (q_row0 >= len) return;
+  const int n_kv = (len + kBN - 1) / kBN;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -123,7 +127,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           tma_load_3d(sm + Ly::kQ + t * Ly::kTile + s * 16384, &tmQ, bar_q + t, head * D + s * 64,
                       q_row0 + t * kBM, seq);
       }
-      for (int j = 0; j < a.n_kv; ++j) {
+      for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
         const uint32_t ph = (j >> 1) & 1;
         mbar_wait(bar_ke + st, ph ^ 1);
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     mbar_wait(bar_q + 0, 0);
     mbar_wait(bar_q + 1, 0);
     tc_fence_after();
-    for (int j = 0; j < a.n_kv; ++j) {
+    for (int j = 0; j < n_kv; ++j) {
       const int st = j & 1;
       const uint32_t ph = (j >> 1) & 1;
       mbar_wait(bar_kf + st, ph);
@@ -196,7 +200,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tc_fence_after();
       pv(0, st, j > 0, nullptr, nullptr, nullptr);
     }
-    const int last = a.n_kv - 1;
+    const int last = n_kv - 1;
     mbar_wait(bar_p + 1, last & 1);
     tc_fence_after();
     pv(1, last & 1, last > 0, bar_ve + (last & 1), bar_o + 0, bar_o + 1);
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // key-mask words of tile j (validity bits and the subsequence tail), fetched one tile ahead
     auto mask_words = [&](int j, uint32_t (&w)[4]) {
       const int kv0 = j * kBN;
-      const int nvalid = min(kBN, a.seq_len - kv0);
+      const int nvalid = min(kBN, len - kv0);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         uint32_t m = vbits ? ((kv0 >> 5) + i < a.words_per_seq ? __ldg(vbits + (kv0 >> 5) + i) : 0u)
@@ -241,11 +245,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     };
     uint32_t w_next[4];
     mask_words(0, w_next);
-    for (int j = 0; j < a.n_kv; ++j) {
+    for (int j = 0; j < n_kv; ++j) {
       uint32_t w[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) w[i] = w_next[i];
-      if (j + 1 < a.n_kv) mask_words(j + 1, w_next);
+      if (j + 1 < n_kv) mask_words(j + 1, w_next);
       mbar_wait(bar_s + t, j & 1);
       tc_fence_after();
       if (a.flags & 2) {
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             ls1 += p1;
             pk[i] = pack_bf16(p0, p1);
           }
-          if (turn && pingpong && cc == 3 && !(t == 1 && j == a.n_kv - 1))
+          if (turn && pingpong && cc == 3 && !(t == 1 && j == n_kv - 1))
             asm volatile("bar.arrive %0, 256;" ::"r"(next_turn) : "memory");
           tmem_st16(tS + cc * 16, pk);
         }
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // ---------------------------------------------------------------- epilogue
     mbar_wait(bar_o + t, 0);
     tc_fence_after();
-    const bool row_ok = q_row < a.seq_len;
+    const bool row_ok = q_row < len;
     bool q_valid = true;
     if (a.zero_invalid_q && vbits && row_ok) q_valid = bit_at(vbits, a.words_per_seq, q_row);
     const bool live = row_ok && q_valid && l > 0.f;
@@ -408,7 +412,7 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
   a.words_per_seq = static_cast<int>((s.seq_len + 31) / 32);
   a.seq_len = static_cast<int>(s.seq_len);
   a.heads = static_cast<int>(s.heads);
-  a.n_kv = static_cast<int>((s.seq_len + kBN - 1) / kBN);
+  a.seq_lens = s.seq_lens;
   a.scale_log2 = scale * 1.4426950408889634f;
   a.zero_invalid_q = zero_invalid_q;
   {

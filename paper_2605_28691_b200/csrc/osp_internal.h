@@ -45,7 +45,8 @@ struct MapParams {
 };
 
 struct AttnShape {
-  int64_t n_seq, seq_len, heads, head_dim;
+  int64_t n_seq, seq_len, heads, head_dim;  // seq_len = capacity (row stride of a sequence)
+  const int32_t* seq_lens = nullptr;         // optional per-sequence valid lengths (<= seq_len)
 };
 
 int launch_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,

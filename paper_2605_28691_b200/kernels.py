@@ -161,11 +161,21 @@ def _head_dim_plan(d: int) -> int:
     raise UnsupportedError(f"head_dim {d} > 128 is not supported by the B200 attention kernels")
 
 
+def _lens(seq_lens, n_seq, seq_len):
+    if seq_lens is None:
+        return None
+    _cuda(seq_lens, "seq_lens")
+    if seq_lens.dtype != torch.int32 or seq_lens.numel() != n_seq:
+        raise ShapeError(f"seq_lens must be ({n_seq},) int32")
+    return seq_lens.contiguous()
+
+
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, heads: int, head_dim: int,
              valid_bits: torch.Tensor | None, zero_invalid_queries: bool, scale: float,
-             out: torch.Tensor | None = None):
+             out: torch.Tensor | None = None, seq_lens: torch.Tensor | None = None):
     """q, k, v: (n_seq, L, >= heads*head_dim) bf16 views with unit column stride.
-    Returns (o (n_seq, L, heads*head_dim) bf16, lse (n_seq, heads, L) fp32)."""
+    Returns (o (n_seq, L, heads*head_dim) bf16, lse (n_seq, heads, L) fp32).  seq_lens
+    (n_seq,) int32: per-sequence lengths <= L (rows beyond are ignored and not written)."""
     L = _lib.lib()
     for name, t in (("q", q), ("k", k), ("v", v)):
         _cuda(t, name)
@@ -177,15 +187,17 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, heads: int, head
     if out is None:
         out = torch.empty((n_seq, seq_len, heads * head_dim), dtype=torch.bfloat16, device=q.device)
     lse = torch.empty((n_seq, heads, seq_len), dtype=torch.float32, device=q.device)
+    lens = _lens(seq_lens, n_seq, seq_len)
     _lib.check(STATS.run('attn_fwd', 1, lambda: L.osp_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                               lse.data_ptr(), n_seq, seq_len, heads, head_dim, q.stride(1),
                               k.stride(1), v.stride(1), out.stride(1), _lib.ptr(valid_bits),
-                              int(zero_invalid_queries), float(scale), _lib.stream_ptr(q.device))))
+                              _lib.ptr(lens), int(zero_invalid_queries), float(scale),
+                              _lib.stream_ptr(q.device))))
     return out, lse
 
 
 def attn_bwd(q, k, v, o, do, lse, heads: int, head_dim: int, valid_bits, zero_invalid_queries: bool,
-             scale: float, dq=None, dk=None, dv=None):
+             scale: float, dq=None, dk=None, dv=None, seq_lens=None):
     L = _lib.lib()
     n_seq, seq_len = q.shape[0], q.shape[1]
     C = heads * head_dim
@@ -200,12 +212,13 @@ def attn_bwd(q, k, v, o, do, lse, heads: int, head_dim: int, valid_bits, zero_in
         dv = torch.empty((n_seq, seq_len, C), dtype=torch.bfloat16, device=dev)
     ws_bytes = L.osp_attn_bwd_workspace_bytes(n_seq, seq_len, heads, head_dim)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    lens = _lens(seq_lens, n_seq, seq_len)
     _lib.check(STATS.run('attn_bwd', 3, lambda: L.osp_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
                               lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), n_seq,
                               seq_len, heads, head_dim, q.stride(1), k.stride(1), v.stride(1),
                               o.stride(1), do.stride(1), dq.stride(1), dk.stride(1), dv.stride(1),
-                              _lib.ptr(valid_bits), int(zero_invalid_queries), float(scale),
-                              ws.data_ptr(), ws_bytes, _lib.stream_ptr(dev))))
+                              _lib.ptr(valid_bits), _lib.ptr(lens), int(zero_invalid_queries),
+                              float(scale), ws.data_ptr(), ws_bytes, _lib.stream_ptr(dev))))
     return dq, dk, dv
 
 

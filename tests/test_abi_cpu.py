@@ -65,8 +65,8 @@ def test_argument_errors_without_gpu(cdll):
     assert rc == 4  # ShardingError k^2 % N
     rc = cdll.osp_ssp_pack(None, None, 2, 8, 2, 3, 1, 4, 4, 2, None)
     assert rc == 6  # ProtocolError local batch % G
-    rc = cdll.osp_attn_fwd(None, None, None, None, None, 1, 128, 1, 96, 96, 96, 96, 96, None, 0,
-                           1.0, None)
+    rc = cdll.osp_attn_fwd(None, None, None, None, None, 1, 128, 1, 96, 96, 96, 96, 96, None, None,
+                           0, 1.0, None)
     assert rc == 8  # unsupported head_dim
 
 

@@ -203,3 +203,37 @@ def test_attention_backward_vs_autograd(lib, n, L, heads, d, masked):
         print(f"bwd d{name} n={n} L={L} h={heads} d={d}: max|err| {e:.3e} rel {rel:.3e} "
               f"(bf16 torch {e_pt:.3e})")
         assert e <= 2 * e_pt + 2e-3, name
+
+
+@pytest.mark.parametrize("lens,heads,d", [((700, 333, 64, 1), 2, 128), ((1000, 513, 0), 1, 64),
+                                          ((2048, 1999), 1, 128)])
+def test_attention_varlen_matches_per_sequence_runs(lib, lens, heads, d):
+    """seq_lens: each sequence attends over its own first len rows only (compacted padding);
+    equals the masked reference with keys >= len invalid, on rows < len, fwd and bwd."""
+    from paper_2605_28691_b200 import kernels
+    n, L = len(lens), max(lens) + 37
+    rng = np.random.default_rng(sum(lens))
+    C = heads * d
+    q, k, v, do = (_bf16(rng.standard_normal((n, L, C))) for _ in range(4))
+    valid = torch.arange(L)[None, :] < torch.tensor(lens)[:, None]
+    sl = torch.tensor(lens, dtype=torch.int32, device=_dev())
+    qd, kd, vd = q.to(_dev()), k.to(_dev()), v.to(_dev())
+    o, lse = kernels.attn_fwd(qd, kd, vd, heads, d, None, False, 1 / math.sqrt(d), seq_lens=sl)
+    dq, dk, dv = kernels.attn_bwd(qd, kd, vd, o, do.to(_dev()), lse, heads, d, None, False,
+                                  1 / math.sqrt(d), seq_lens=sl)
+    leaves = [t.double().requires_grad_() for t in (q, k, v)]
+    ref = attention_ref(*leaves, heads, valid, True)
+    gmask = valid[:, :, None].double()
+    ref.backward(do.double() * gmask)         # rows >= len carry no gradient
+    lp = [t.detach().clone().requires_grad_() for t in (q, k, v)]
+    pt = attention_ref(*lp, heads, valid, True, upcast=False)
+    pt.backward(do * gmask.to(do.dtype))
+    m = valid[:, :, None]
+    e = ((o.cpu().double() - ref.detach()).abs() * m).max().item()
+    e_pt = ((pt.detach().double() - ref.detach()).abs() * m).max().item()
+    assert e <= 2 * e_pt + 1e-3, ("fwd", e, e_pt)
+    for name, got, r, p in zip("qkv", (dq, dk, dv), leaves, lp):
+        e = ((got.cpu().double() - r.grad).abs() * m).max().item()
+        e_pt = ((p.grad.double() - r.grad).abs() * m).max().item()
+        assert e <= 2 * e_pt + 2e-3, (name, e, e_pt)
+    assert (dq.cpu()[~valid] == 0).all()       # dq rows beyond a sequence's length are zero
