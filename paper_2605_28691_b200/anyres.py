@@ -68,6 +68,24 @@ class PaddedGrid:
         return self._cache[key]
 
 
+    def compact_plan(self, pattern: SparsePattern, batch: int = 1, rows: tuple | None = None):
+        """CompactPlan (compact.py) of the pattern layout's subsequences [rows[0], rows[1]) of
+        the enlarged batch (all when None); None when the grid needs no padding."""
+        if self.trivial:
+            return None
+        key = ("plan", pattern, batch, rows)
+        if key not in self._cache:
+            from .compact import compact_plan
+            p = self.padded
+            L = p.seq_len if pattern is SparsePattern.ORIGINAL else p.seq_len // (p.k * p.k)
+            bits = self.mask_bits(pattern, batch)
+            valid = kernels.bits_to_bytes(bits, L).view(-1, L).bool()
+            if rows is not None:
+                valid = valid[rows[0]:rows[1]]
+            self._cache[key] = compact_plan(valid)
+        return self._cache[key]
+
+
 def pad_grid(g: GridShape) -> PaddedGrid:
     """Pad h and w to the nearest multiple of k^2; t is never padded (anyres.py:57-66)."""
     k2 = g.k * g.k

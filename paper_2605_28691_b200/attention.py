@@ -72,41 +72,43 @@ class _AttnPacked(torch.autograd.Function):
     writes dq, dk, dv straight into one packed gradient buffer."""
 
     @staticmethod
-    def forward(ctx, qkv, heads, d, bits, zero_q, scale):
+    def forward(ctx, qkv, heads, d, bits, zero_q, scale, seq_lens=None):
         C = heads * d
         q, k, v = qkv[..., :C], qkv[..., C:2 * C], qkv[..., 2 * C:]
-        o, lse = kernels.attn_fwd(q, k, v, heads, d, bits, zero_q, scale)
+        o, lse = kernels.attn_fwd(q, k, v, heads, d, bits, zero_q, scale, seq_lens=seq_lens)
         ctx.save_for_backward(qkv, o, lse)
-        ctx.cfg = (heads, d, bits, zero_q, scale)
+        ctx.cfg = (heads, d, bits, zero_q, scale, seq_lens)
         return o
 
     @staticmethod
     def backward(ctx, do):
         qkv, o, lse = ctx.saved_tensors
-        heads, d, bits, zero_q, scale = ctx.cfg
+        heads, d, bits, zero_q, scale, seq_lens = ctx.cfg
         C = heads * d
-        dqkv = torch.empty_like(qkv)
+        # with seq_lens, dk / dv rows beyond a sequence's length are not written: start from 0
+        dqkv = torch.zeros_like(qkv) if seq_lens is not None else torch.empty_like(qkv)
         kernels.attn_bwd(qkv[..., :C], qkv[..., C:2 * C], qkv[..., 2 * C:], o, do.contiguous(), lse,
                          heads, d, bits, zero_q, scale, dq=dqkv[..., :C], dk=dqkv[..., C:2 * C],
-                         dv=dqkv[..., 2 * C:])
-        return dqkv, None, None, None, None, None
+                         dv=dqkv[..., 2 * C:], seq_lens=seq_lens)
+        return dqkv, None, None, None, None, None, None
 
 
 class _Attn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, heads, d, bits, zero_q, scale):
-        o, lse = kernels.attn_fwd(q, k, v, heads, d, bits, zero_q, scale)
+    def forward(ctx, q, k, v, heads, d, bits, zero_q, scale, seq_lens=None):
+        o, lse = kernels.attn_fwd(q, k, v, heads, d, bits, zero_q, scale, seq_lens=seq_lens)
         ctx.save_for_backward(q, k, v, o, lse)
-        ctx.cfg = (heads, d, bits, zero_q, scale)
+        ctx.cfg = (heads, d, bits, zero_q, scale, seq_lens)
         return o
 
     @staticmethod
     def backward(ctx, do):
         q, k, v, o, lse = ctx.saved_tensors
-        heads, d, bits, zero_q, scale = ctx.cfg
+        heads, d, bits, zero_q, scale, seq_lens = ctx.cfg
+        z = (lambda t: torch.zeros_like(t)) if seq_lens is not None else (lambda t: None)
         dq, dk, dv = kernels.attn_bwd(q, k, v, o, do.contiguous(), lse, heads, d, bits, zero_q,
-                                      scale)
-        return dq, dk, dv, None, None, None, None, None
+                                      scale, dq=z(q), dk=z(k), dv=z(v), seq_lens=seq_lens)
+        return dq, dk, dv, None, None, None, None, None, None
 
 
 def _pad_heads(t: torch.Tensor, heads: int, d: int, dp: int) -> torch.Tensor:
@@ -115,8 +117,9 @@ def _pad_heads(t: torch.Tensor, heads: int, d: int, dp: int) -> torch.Tensor:
 
 
 def attention_packed(qkv: torch.Tensor, heads: int, bits=None, zero_invalid_queries=False,
-                     scale: float | None = None) -> torch.Tensor:
-    """Per-item attention over packed bf16 [q | k | v] (n_seq, L, 3*C) -> (n_seq, L, C)."""
+                     scale: float | None = None, seq_lens: torch.Tensor | None = None) -> torch.Tensor:
+    """Per-item attention over packed bf16 [q | k | v] (n_seq, L, 3*C) -> (n_seq, L, C).
+    seq_lens (n_seq,) int32: item s uses only its first seq_lens[s] rows (compacted padding)."""
     C = qkv.shape[-1] // 3
     d = C // heads
     if heads * d != C:
@@ -125,10 +128,10 @@ def attention_packed(qkv: torch.Tensor, heads: int, bits=None, zero_invalid_quer
     dp = kernels._head_dim_plan(d)
     if dp == d:
         return _AttnPacked.apply(qkv.contiguous(), heads, d, bits, bool(zero_invalid_queries),
-                                 scale)
+                                 scale, seq_lens)
     q, k, v = (_pad_heads(qkv[..., i * C:(i + 1) * C], heads, d, dp) for i in range(3))
     o = _Attn.apply(q.contiguous(), k.contiguous(), v.contiguous(), heads, dp, bits,
-                    bool(zero_invalid_queries), scale)
+                    bool(zero_invalid_queries), scale, seq_lens)
     n, L, _ = o.shape
     return o.reshape(n, L, heads, dp)[..., :d].reshape(n, L, C)
 
@@ -191,14 +194,20 @@ def skiparse_attention(x, g: GridShape, pattern: SparsePattern, pg: PaddedGrid |
     if C % heads:
         raise ShapeError(f"chan {C} not divisible by heads {heads}")
     W = weights if weights is not None else packed_projection(C, COMPUTE_DTYPE, xd.device)
-    bits = pg.mask_bits(pattern, B) if pg is not None else None
     xb = xd.to(COMPUTE_DTYPE)
     if pattern is SparsePattern.ORIGINAL:
         xp = xb
     else:
         xp = pattern_map(grid, pattern, B).apply(xb)
-    qkv = torch.matmul(xp, W)
-    o = attention_packed(qkv, heads, bits, zero_invalid_queries=bits is not None)
+    plan = pg.compact_plan(pattern, B) if pg is not None else None
+    if plan is None:
+        o = attention_packed(torch.matmul(xp, W), heads)
+    else:
+        # pad tokens are masked keys and zero-output queries (attention.py:121-130): run only the
+        # real rows of each subsequence (compact.py) -- identical values, less work
+        from .compact import compact_rows, expand_rows
+        qkv = torch.matmul(compact_rows(xp, plan), W)
+        o = expand_rows(attention_packed(qkv, heads, seq_lens=plan.lens), plan)
     if pattern is not SparsePattern.ORIGINAL:
         o = inverse_pattern_map(grid, pattern, B).apply(o)
     out = o.to(xd.dtype)

@@ -49,7 +49,7 @@ class SkiparseBlock:
     def __init__(self, g: GridShape, heads: int, chan: int, batch: int = 1, group=None,
                  log: CommLog | None = None, device=None, seeds=(PROJECTION_SEED, PROJECTION_SEED + 1),
                  transport: str = "native", qk_norm: str | None = None, rope: bool = False,
-                 eps: float = 1e-6):
+                 eps: float = 1e-6, compact: bool = True):
         import torch.distributed as dist
         self.g = g
         self.pg: PaddedGrid = pad_grid(g)
@@ -84,6 +84,9 @@ class SkiparseBlock:
         bg = self.pg.mask_bits(SparsePattern.GROUP_WISE, batch)
         self.bits_tsa = None if bt is None else bt[r0:r1].contiguous()
         self.bits_gsa = None if bg is None else bg[r0:r1].contiguous()
+        # padding compaction (compact.py): attention over each subsequence's real rows only
+        self.plan_tsa = self.pg.compact_plan(SparsePattern.TOKEN_WISE, batch, (r0, r1)) if compact else None
+        self.plan_gsa = self.pg.compact_plan(SparsePattern.GROUP_WISE, batch, (r0, r1)) if compact else None
         self._t2g = IndexMap._pattern("tsa_to_gsa", self.grid, batch)
         self._g2t = IndexMap._pattern("gsa_to_tsa", self.grid, batch)
 
@@ -99,14 +102,23 @@ class SkiparseBlock:
         return ssp_switch(x, self.grid, self.group, self.log, self.transport)
 
     def attend(self, x, W, bits, pattern=SparsePattern.TOKEN_WISE):
+        from .compact import compact_rows, expand_rows
+        plan = self.plan_tsa if pattern is SparsePattern.TOKEN_WISE else self.plan_gsa
         if self.prologue:
             from .prologue import QKVPrologue
             Wt = self.W1t if W is self.W1 else self.W2t
+            # RoPE positions come from padded-layout rows: project first, then compact
             qkv = QKVPrologue.apply(x, self.grid, pattern, self.batch, self.qk_norm, self.gamma_q,
                                     self.gamma_k, self.eps, self.rope,
                                     self.rank * self.local_rows * self.L, Wt)
+            if plan is not None:
+                qkv = compact_rows(qkv, plan)
+        elif plan is not None:
+            qkv = torch.matmul(compact_rows(x, plan), W)
         else:
             qkv = torch.matmul(x, W)
+        if plan is not None:
+            return expand_rows(attention_packed(qkv, self.heads, seq_lens=plan.lens), plan)
         return attention_packed(qkv, self.heads, bits, zero_invalid_queries=bits is not None)
 
     def __call__(self, x_tsa: torch.Tensor) -> torch.Tensor:
@@ -127,15 +139,27 @@ class SkiparseBlock:
         return full[r0:r0 + self.local_rows]
 
     def flops(self) -> dict:
-        """Algorithmic tensor FLOPs of one block fwd+bwd for this rank, counted on
-        the padded grid as the reference's flop_report is (checks.py:144-146)."""
+        """Tensor FLOPs of one block fwd+bwd for this rank.  `attention_fwd_per_app` counts the
+        padded grid as the reference's flop_report does (checks.py:144-146); the `executed`
+        counts are what the kernels run -- with padding compaction exactly the real-token
+        ("useful") interactions."""
         d = self.chan // self.heads
         att_fwd = 4 * self.local_rows * self.L * self.L * d * self.heads  # per application
         rows = self.local_rows * self.L
-        proj_fwd = 2 * rows * self.chan * 3 * self.chan  # x @ [Wq|Wk|Wv]
+
+        def executed(plan):
+            if plan is None:
+                return att_fwd, rows
+            lens = plan.lens.to(torch.int64)
+            return int((lens * lens).sum()) * 4 * d * self.heads, int(lens.sum())
+
+        (f1, r1), (f2, r2) = executed(self.plan_tsa), executed(self.plan_gsa)
+        proj = 2 * self.chan * 3 * self.chan  # per row: x @ [Wq|Wk|Wv]
+        proj_rows = 2 * rows if self.prologue or self.plan_tsa is None else r1 + r2
         return {
             "attention_fwd_per_app": att_fwd,
-            "attention_fwd_bwd": 2 * 3.5 * att_fwd,
-            "projection_fwd_bwd": 2 * 2 * proj_fwd,  # fwd GEMM + input-gradient GEMM
-            "total": 2 * 3.5 * att_fwd + 4 * proj_fwd,
+            "attention_fwd_executed": f1 + f2,           # both applications
+            "attention_fwd_bwd": 3.5 * (f1 + f2),
+            "projection_fwd_bwd": 2 * proj * proj_rows,  # fwd GEMM + input-gradient GEMM
+            "total": 3.5 * (f1 + f2) + 2 * proj * proj_rows,
         }

@@ -1,0 +1,91 @@
+"""Padding compaction for the attention (a B200-first restatement of the reference's masking).
+
+On an any-resolution grid the reference pads H, W to multiples of k^2 and then *masks* the pad
+tokens inside every subsequence (anyres.py:92-96, attention.py:121-130): pad keys weigh 0 and
+pad queries output 0.  Computing those rows and then discarding them costs (S_pad / S_real)^2
+of the attention work (1.14x at 720p, 45 -> 48 rows).  Here each subsequence's real rows are
+gathered into a compact buffer (K1 table gather), attention runs with per-subsequence lengths
+(K2/K3 `seq_lens`), and the outputs are scattered back with zero pad rows -- the same values the
+masked computation produces, for ~12% less tensor work at 720p.  Both moves are exact
+permutations whose adjoints are each other, so autograd is a gather with the other table.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import kernels
+
+__all__ = ["CompactPlan", "compact_plan", "compact_rows", "expand_rows"]
+
+
+@dataclass(frozen=True)
+class CompactPlan:
+    n_seq: int
+    L: int                  # padded subsequence length
+    cap: int                # longest compacted subsequence (buffer capacity)
+    lens: torch.Tensor      # (n_seq,) int32 real rows per subsequence
+    gather: torch.Tensor    # (n_seq*cap,) int64 padded row of each compact row, -1 = empty
+    scatter: torch.Tensor   # (n_seq*L,) int64 compact row of each padded row, -1 = pad
+
+    @property
+    def real_rows(self) -> int:
+        return int(self.lens.sum())
+
+
+def compact_plan(valid: torch.Tensor) -> CompactPlan:
+    """valid: (n_seq, L) bool on the device (True = real token)."""
+    n_seq, L = valid.shape
+    v = valid.to(torch.bool)
+    lens = v.sum(dim=1)
+    cap = max(int(lens.max().item()) if n_seq else 0, 1)
+    j = torch.cumsum(v.to(torch.int64), dim=1) - 1
+    s = torch.arange(n_seq, device=v.device, dtype=torch.int64)[:, None]
+    pos = torch.arange(L, device=v.device, dtype=torch.int64)[None, :]
+    scatter = torch.where(v, s * cap + j, torch.full_like(j, -1))
+    gather = torch.full((n_seq * cap,), -1, dtype=torch.int64, device=v.device)
+    gather[scatter[v]] = (s * L + pos).expand(n_seq, L)[v]
+    return CompactPlan(n_seq, L, cap, lens.to(torch.int32).contiguous(), gather.contiguous(),
+                       scatter.reshape(-1).contiguous())
+
+
+def _move(x: torch.Tensor, index: torch.Tensor, n_rows: int, rows_per_seq: int) -> torch.Tensor:
+    C = x.shape[-1]
+    out = kernels.gather_rows(x.reshape(-1, C), index, n_rows)
+    return out.view(n_rows // rows_per_seq, rows_per_seq, C)
+
+
+class _Compact(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, plan):
+        ctx.plan = plan
+        return _move(x, plan.gather, plan.n_seq * plan.cap, plan.cap)
+
+    @staticmethod
+    def backward(ctx, g):
+        p = ctx.plan
+        return _move(g.contiguous(), p.scatter, p.n_seq * p.L, p.L), None
+
+
+class _Expand(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, y, plan):
+        ctx.plan = plan
+        return _move(y, plan.scatter, plan.n_seq * plan.L, plan.L)
+
+    @staticmethod
+    def backward(ctx, g):
+        p = ctx.plan
+        return _move(g.contiguous(), p.gather, p.n_seq * p.cap, p.cap), None
+
+
+def compact_rows(x: torch.Tensor, plan: CompactPlan) -> torch.Tensor:
+    """(n_seq, L, C) padded pattern layout -> (n_seq, cap, C) real rows first."""
+    return _Compact.apply(x, plan)
+
+
+def expand_rows(y: torch.Tensor, plan: CompactPlan) -> torch.Tensor:
+    """(n_seq, cap, C) -> (n_seq, L, C) with zero pad rows."""
+    return _Expand.apply(y, plan)

@@ -139,6 +139,13 @@ class HybridStack:
             b = self.pg.mask_bits(pat, batch)
             self.bits[pat] = None if b is None else b[r0:r0 + self.local_rows].contiguous()
             self.full_bits[pat] = None if b is None else full_sequence_bits(b, k2, batch, self.L)
+        # padding compaction (compact.py): attention over real rows only, for both block kinds
+        from .compact import compact_plan
+        self.plans = {pat: self.pg.compact_plan(pat, batch, (r0, r0 + self.local_rows))
+                      for pat in (SparsePattern.TOKEN_WISE, SparsePattern.GROUP_WISE)}
+        self.full_plans = {pat: None if fb is None else
+                           compact_plan(kernels.bits_to_bytes(fb, k2 * self.L).view(batch, -1))
+                           for pat, fb in self.full_bits.items()}
         self._t2g = IndexMap._pattern("tsa_to_gsa", self.grid, batch)
         self._g2t = IndexMap._pattern("gsa_to_tsa", self.grid, batch)
 
@@ -149,9 +156,12 @@ class HybridStack:
         return ssp_switch(x, self.grid, self.group, self.log)
 
     def _skiparse(self, x, W, pat):
-        qkv = torch.matmul(x, W)
-        bits = self.bits[pat]
-        return attention_packed(qkv, self.heads, bits, zero_invalid_queries=bits is not None)
+        from .compact import compact_rows, expand_rows
+        plan = self.plans[pat]
+        if plan is not None:
+            qkv = torch.matmul(compact_rows(x, plan), W)
+            return expand_rows(attention_packed(qkv, self.heads, seq_lens=plan.lens), plan)
+        return attention_packed(torch.matmul(x, W), self.heads)
 
     def _full(self, x, W, pat):
         """Full attention over each batch item's whole (padded) sequence, computed in the
@@ -165,7 +175,13 @@ class HybridStack:
         B = self.batch
         # rows are nested (pattern id, batch item): regroup to one sequence per batch item
         seq = qkv.view(self.n_sub, B, L, C3).transpose(0, 1).reshape(B, self.n_sub * L, C3)
-        o = attention_packed(seq, self.heads // n, bits, zero_invalid_queries=bits is not None)
+        plan = self.full_plans[pat]
+        if plan is not None:
+            from .compact import compact_rows, expand_rows
+            o = expand_rows(attention_packed(compact_rows(seq, plan), self.heads // n,
+                                             seq_lens=plan.lens), plan)
+        else:
+            o = attention_packed(seq, self.heads // n, bits, zero_invalid_queries=bits is not None)
         o = o.view(B, self.n_sub, L, C3 // 3).transpose(0, 1).reshape(rows, L, C3 // 3)
         if n > 1:
             o = _UlyssesOut.apply(o, n, self.group, self.log)
@@ -187,11 +203,20 @@ class HybridStack:
         return x
 
     def flops(self) -> dict:
+        """Executed attention FLOPs (real-token interactions when the grid is padded)."""
         d = self.chan // self.heads
-        n_rows = self.local_rows
-        sk = 4 * n_rows * self.L * self.L * d * self.heads
+
+        def sq(plan, default):
+            if plan is None:
+                return default
+            lens = plan.lens.to(torch.int64)
+            return int((lens * lens).sum())
+
+        sk = 4 * d * self.heads * sq(self.plans[SparsePattern.TOKEN_WISE],
+                                     self.local_rows * self.L * self.L)
         S = self.n_sub * self.L
-        full = 4 * self.batch * S * S * d * self.heads // self.world
+        full = 4 * d * self.heads * sq(self.full_plans[SparsePattern.TOKEN_WISE],
+                                       self.batch * S * S) // self.world
         n_full = sum(1 for s in self.schedule if s is LayerKind.FULL)
         n_sk = len(self.schedule) - n_full
         return {"attention_fwd": n_full * full + n_sk * sk,
