@@ -89,6 +89,19 @@ class SkiparseBlock:
         self.plan_gsa = self.pg.compact_plan(SparsePattern.GROUP_WISE, batch, (r0, r1)) if compact else None
         self._t2g = IndexMap._pattern("tsa_to_gsa", self.grid, batch)
         self._g2t = IndexMap._pattern("gsa_to_tsa", self.grid, batch)
+        # one GPU with compaction: fold expand -> pattern switch -> compact into one row move
+        # each way (compact TSA -> compact GSA, compact GSA -> padded TSA)
+        self._fused = None
+        if self.world == 1 and self.plan_tsa is not None and not (qk_norm is not None or rope):
+            from .compact import row_move
+            pt, pgs = self.plan_tsa, self.plan_gsa
+            t2g = self._t2g.src.reshape(-1)                 # padded GSA row <- padded TSA row
+            g2t = self._g2t.src.reshape(-1)
+            gp = pgs.gather                                  # compact GSA row -> padded GSA row
+            a = torch.where(gp >= 0, pt.scatter[t2g[gp.clamp(min=0)]], torch.full_like(gp, -1))
+            b = pgs.scatter[g2t]                             # padded TSA row <- compact GSA row
+            self._fused = (row_move(a, pt.n_seq * pt.cap, pgs.cap, pt.cap),
+                           row_move(b, pgs.n_seq * pgs.cap, pt.L, pgs.cap))
 
     # ------------------------------------------------------------------ pieces
     def switch_to_gsa(self, x):
@@ -121,8 +134,18 @@ class SkiparseBlock:
             return expand_rows(attention_packed(qkv, self.heads, seq_lens=plan.lens), plan)
         return attention_packed(qkv, self.heads, bits, zero_invalid_queries=bits is not None)
 
+    def _call_fused(self, x_tsa):
+        from .compact import apply_move, compact_rows
+        pt, pgs = self.plan_tsa, self.plan_gsa
+        o1 = attention_packed(torch.matmul(compact_rows(x_tsa, pt), self.W1), self.heads, seq_lens=pt.lens)
+        x2 = apply_move(o1, self._fused[0])
+        o2 = attention_packed(torch.matmul(x2, self.W2), self.heads, seq_lens=pgs.lens)
+        return apply_move(o2, self._fused[1])
+
     def __call__(self, x_tsa: torch.Tensor) -> torch.Tensor:
         """x_tsa: this rank's (G*B, L, C) bf16 shard in the token-wise layout."""
+        if self._fused is not None:
+            return self._call_fused(x_tsa)
         o1 = self.attend(x_tsa, self.W1, self.bits_tsa)
         x2 = self.switch_to_gsa(o1)
         o2 = self.attend(x2, self.W2, self.bits_gsa, SparsePattern.GROUP_WISE)

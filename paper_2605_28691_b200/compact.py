@@ -18,7 +18,7 @@ import torch
 
 from . import kernels
 
-__all__ = ["CompactPlan", "compact_plan", "compact_rows", "expand_rows"]
+__all__ = ["CompactPlan", "compact_plan", "compact_rows", "expand_rows", "RowMove", "row_move"]
 
 
 @dataclass(frozen=True)
@@ -89,3 +89,38 @@ def compact_rows(x: torch.Tensor, plan: CompactPlan) -> torch.Tensor:
 def expand_rows(y: torch.Tensor, plan: CompactPlan) -> torch.Tensor:
     """(n_seq, cap, C) -> (n_seq, L, C) with zero pad rows."""
     return _Expand.apply(y, plan)
+
+
+@dataclass(frozen=True)
+class RowMove:
+    """An injective row move out[i] = in[src[i]] (src = -1 -> zero row) between two
+    (n_seq, rows_per_seq, C) layouts, with its adjoint (the inverse table)."""
+
+    src: torch.Tensor       # (n_out_seq*out_rows,) int64
+    inv: torch.Tensor       # (n_in_seq*in_rows,) int64
+    out_rows: int
+    in_rows: int
+
+
+def row_move(src: torch.Tensor, n_in_total: int, out_rows: int, in_rows: int) -> RowMove:
+    src = src.to(torch.int64).contiguous()
+    inv = torch.full((n_in_total,), -1, dtype=torch.int64, device=src.device)
+    ok = src >= 0
+    inv[src[ok]] = torch.nonzero(ok).view(-1)
+    return RowMove(src, inv, out_rows, in_rows)
+
+
+class _Move(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, mv):
+        ctx.mv = mv
+        return _move(x, mv.src, mv.src.numel(), mv.out_rows)
+
+    @staticmethod
+    def backward(ctx, g):
+        mv = ctx.mv
+        return _move(g.contiguous(), mv.inv, mv.inv.numel(), mv.in_rows), None
+
+
+def apply_move(x: torch.Tensor, mv: RowMove) -> torch.Tensor:
+    return _Move.apply(x, mv)
