@@ -109,8 +109,8 @@ int osp_mask_bits_to_bytes(const uint32_t* bits, uint8_t* valid, int64_t n_rows,
  *   valid_bits: NULL or (n_seq, ceil(seq_len/32)) key validity (attention.py:35-44 rules:
  *             masked keys weigh 0, an all-masked row outputs 0).
  *   seq_lens: NULL or (n_seq) int32 per-sequence lengths <= seq_len: sequence s uses only its
- *             first seq_lens[s] rows as queries and keys (rows beyond are not read as keys and
- *             not written).  This runs subsequences with their padding compacted away.
+ *             first seq_lens[s] rows as queries and keys; its rows beyond get o = 0, lse = +inf.
+ *             This runs subsequences with their padding compacted away.
  *   zero_invalid_queries: rows whose own bit is 0 output 0 (attention.py:127-130).
  *   scale   : softmax scale (reference: 1/sqrt(chan) with one head, attention.py:57).
  */
@@ -121,8 +121,8 @@ int osp_attn_fwd(const void* q, const void* k, const void* v, void* o, float* ls
 
 /*
  * K3: backward of osp_attn_fwd (no reference counterpart: attention.py has no backward).
- * Writes dq, dk, dv (bf16, own row strides; with seq_lens, rows beyond a sequence's length get
- * dq = 0 and dk, dv untouched).  workspace >= osp_attn_bwd_workspace_bytes().
+ * Writes dq, dk, dv (bf16, own row strides; with seq_lens, rows beyond a sequence's length are
+ * 0).  workspace >= osp_attn_bwd_workspace_bytes().
  */
 size_t osp_attn_bwd_workspace_bytes(int64_t n_seq, int64_t seq_len, int64_t heads,
                                     int64_t head_dim);

@@ -85,8 +85,7 @@ class _AttnPacked(torch.autograd.Function):
         qkv, o, lse = ctx.saved_tensors
         heads, d, bits, zero_q, scale, seq_lens = ctx.cfg
         C = heads * d
-        # with seq_lens, dk / dv rows beyond a sequence's length are not written: start from 0
-        dqkv = torch.zeros_like(qkv) if seq_lens is not None else torch.empty_like(qkv)
+        dqkv = torch.empty_like(qkv)
         kernels.attn_bwd(qkv[..., :C], qkv[..., C:2 * C], qkv[..., 2 * C:], o, do.contiguous(), lse,
                          heads, d, bits, zero_q, scale, dq=dqkv[..., :C], dk=dqkv[..., C:2 * C],
                          dv=dqkv[..., 2 * C:], seq_lens=seq_lens)
@@ -105,9 +104,8 @@ class _Attn(torch.autograd.Function):
     def backward(ctx, do):
         q, k, v, o, lse = ctx.saved_tensors
         heads, d, bits, zero_q, scale, seq_lens = ctx.cfg
-        z = (lambda t: torch.zeros_like(t)) if seq_lens is not None else (lambda t: None)
         dq, dk, dv = kernels.attn_bwd(q, k, v, o, do.contiguous(), lse, heads, d, bits, zero_q,
-                                      scale, dq=z(q), dk=z(k), dv=z(v), seq_lens=seq_lens)
+                                      scale, seq_lens=seq_lens)
         return dq, dk, dv, None, None, None, None, None, None
 
 

@@ -123,7 +123,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int seq = blockIdx.z;
   const int kv0 = blockIdx.x * 128;
   const int len = a.seq_lens ? __ldg(a.seq_lens + seq) : a.seq_len;
-  if (kv0 >= len) return;
+  if (kv0 >= len) {  // whole key tile past the sequence: dk, dv rows 0
+    const int r1 = min(kv0 + 128, a.seq_len);
+    const int64_t hoff = static_cast<int64_t>(head) * D;
+    zero_rows_bf16(a.dv + static_cast<int64_t>(seq) * a.seq_len * a.dv_stride + hoff, a.dv_stride, kv0, r1, D);
+    zero_rows_bf16(a.dk + static_cast<int64_t>(seq) * a.seq_len * a.dk_stride + hoff, a.dk_stride, kv0, r1, D);
+    return;
+  }
   const int n_q = (len + 127) / 128;
 
   if ((smem_u32(sm) & 1023) != 0) __trap();
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ---------------------------------------------------------------- dK / dV epilogue
     mbar_wait(bar_fin, 0);
     tc_fence_after();
-    const bool row_ok = kglob < len;
+    const bool row_ok = kglob < a.seq_len;  // rows in [len, cap) hold exact zeros
     __nv_bfloat16* dvrow = a.dv + (static_cast<int64_t>(seq) * a.seq_len + kglob) * a.dv_stride +
                            static_cast<int64_t>(head) * D;
     __nv_bfloat16* dkrow = a.dk + (static_cast<int64_t>(seq) * a.seq_len + kglob) * a.dk_stride +
@@ -463,7 +469,13 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
   const int seq = blockIdx.z;
   const int kv0 = blockIdx.x * 128;
   const int len = a.seq_lens ? __ldg(a.seq_lens + seq) : a.seq_len;
-  if (kv0 >= len) return;
+  if (kv0 >= len) {  // whole key tile past the sequence: dk, dv rows 0
+    const int r1 = min(kv0 + 128, a.seq_len);
+    const int64_t hoff = static_cast<int64_t>(head) * D;
+    zero_rows_bf16(a.dv + static_cast<int64_t>(seq) * a.seq_len * a.dv_stride + hoff, a.dv_stride, kv0, r1, D);
+    zero_rows_bf16(a.dk + static_cast<int64_t>(seq) * a.seq_len * a.dk_stride + hoff, a.dk_stride, kv0, r1, D);
+    return;
+  }
   const int n_q = (len + 63) / 64;
 
   if ((smem_u32(sm) & 1023) != 0) __trap();
@@ -733,7 +745,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
     // (warpgroup 0 drains dV, warpgroup 1 drains dK)
     mbar_wait(bar_fin, 0);
     tc_fence_after();
-    const bool row_ok = kglob < len;
+    const bool row_ok = kglob < a.seq_len;  // rows in [len, cap) hold exact zeros
     {
       const int which = half;
       const uint32_t base = (which == 0 ? tDV : tDK) + la;

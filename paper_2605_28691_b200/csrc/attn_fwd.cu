@@ -87,7 +87,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int q_row0 = blockIdx.x * 2 * kBM;
   // variable-length sequences: rows >= len are neither keys nor queries (compacted layouts)
   const int len = a.seq_lens ? __ldg(a.seq_lens + seq) : a.seq_len;
-  if (q_row0 >= len) return;
+  if (q_row0 >= len) {  // whole CTA past the sequence: o rows 0, lse +inf
+    const int r1 = min(q_row0 + 2 * kBM, a.seq_len);
+    zero_rows_bf16(a.o + static_cast<int64_t>(seq) * a.seq_len * a.o_stride + static_cast<int64_t>(head) * D,
+                   a.o_stride, q_row0, r1, D);
+    for (int r = q_row0 + static_cast<int>(threadIdx.x); r < r1; r += blockDim.x)
+      a.lse[(static_cast<int64_t>(seq) * a.heads + head) * a.seq_len + r] = INFINITY;
+    return;
+  }
   const int n_kv = (len + kBN - 1) / kBN;
 
   if (threadIdx.x == 0) {
@@ -357,6 +364,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     mbar_wait(bar_o + t, 0);
     tc_fence_after();
     const bool row_ok = q_row < len;
+    const bool in_cap = q_row < a.seq_len;  // rows in [len, cap) are written as 0 / +inf
     bool q_valid = true;
     if (a.zero_invalid_q && vbits && row_ok) q_valid = bit_at(vbits, a.words_per_seq, q_row);
     const bool live = row_ok && q_valid && l > 0.f;
@@ -368,7 +376,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       uint32_t o[32];
       tmem_ld32(tO + cc * 32, o);
       tmem_wait_ld(o);
-      if (row_ok) {
+      if (in_cap) {
         uint4 pk[4];
         uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
 #pragma unroll
@@ -379,7 +387,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int i = 0; i < 4; ++i) dst[i] = pk[i];
       }
     }
-    if (row_ok) {
+    if (in_cap) {
       const float ms = (m_used == -INFINITY) ? 0.f : m_used * c;
       a.lse[(static_cast<int64_t>(seq) * a.heads + head) * a.seq_len + q_row] =
           live ? (ms + __log2f(l)) * kLn2 : INFINITY;

@@ -53,6 +53,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Zero rows [r0, r1) x `cols` bf16 of a row-strided matrix with all threads of the CTA (rows
+// beyond a sequence's length in the variable-length attention kernels).
+__device__ __forceinline__ void zero_rows_bf16(__nv_bfloat16* base, int64_t stride, int r0, int r1,
+                                               int cols) {
+  const int per_row = cols / 8;  // 16-byte chunks
+  for (int i = threadIdx.x; i < (r1 - r0) * per_row; i += blockDim.x)
+    reinterpret_cast<uint4*>(base + static_cast<int64_t>(r0 + i / per_row) * stride)[i % per_row] =
+        make_uint4(0u, 0u, 0u, 0u);
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

@@ -236,4 +236,6 @@ def test_attention_varlen_matches_per_sequence_runs(lib, lens, heads, d):
         e = ((got.cpu().double() - r.grad).abs() * m).max().item()
         e_pt = ((p.grad.double() - r.grad).abs() * m).max().item()
         assert e <= 2 * e_pt + 2e-3, (name, e, e_pt)
-    assert (dq.cpu()[~valid] == 0).all()       # dq rows beyond a sequence's length are zero
+    for t in (o, dq, dk, dv):                  # rows beyond a sequence's length are zero
+        assert (t.cpu()[~valid] == 0).all()
+    assert torch.isinf(lse.cpu().transpose(1, 2)[~valid]).all()
