@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-    regs_dec<88>();
+    regs_dec<56>();
   if (warp == 0) {
     if (elect_one()) {
       // ------------------------------------------------------------ TMA producer
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     __syncwarp();
   }
   } else {
-    regs_inc<208>();
+    regs_inc<224>();
     // -------------------------------------------------------------- softmax / epilogue
     const int t = (warp - 4) >> 2;
     const int wq = warp & 3;
