@@ -135,6 +135,28 @@ int osp_attn_bwd(const void* q, const void* k, const void* v, const void* o, con
                  size_t workspace_bytes, void* stream);
 
 /*
+ * K2/K3 with the Skiparse Rearrange fused into the TMA prologue / epilogue (gather mode): q, k,
+ * v, o, dout, dq, dk, dv are (n_rows, >= heads*head_dim) row-strided tensors in ANY token layout
+ * (e.g. the original, unpadded latent); sequence s (a subsequence of a pattern) consists of rows
+ * row_index[s*capacity + j], j < seq_lens[s] (entries beyond are -1).  Q/K/V/dO tiles are fetched
+ * with tile::gather4 TMA loads and O, dK, dV, dQ rows are stored through the same table, so no
+ * rearranged copy of the activations ever lands in HBM.  lse is (n_seq, heads, capacity) in
+ * sequence order.  capacity % 4 == 0; the backward needs head_dim 128.
+ */
+int osp_attn_fwd_gather(const void* q, const void* k, const void* v, void* o, float* lse,
+                        int64_t n_rows, const int32_t* row_index, const int32_t* seq_lens,
+                        int64_t n_seq, int64_t capacity, int64_t heads, int64_t head_dim,
+                        int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t o_stride,
+                        float scale, void* stream);
+int osp_attn_bwd_gather(const void* q, const void* k, const void* v, const void* o,
+                        const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                        int64_t n_rows, const int32_t* row_index, const int32_t* seq_lens,
+                        int64_t n_seq, int64_t capacity, int64_t heads, int64_t head_dim,
+                        int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t o_stride,
+                        int64_t do_stride, int64_t dq_stride, int64_t dk_stride, int64_t dv_stride,
+                        float scale, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * K4: Sparse Sequence Parallel pattern switch, local steps of ssp_pattern_switch
  * (ssp.py:139-180; Alg. 1).  One rank's shard is (local_batch, L, chan) with
  * L = t*h*w/k^2, local_batch = G*b, G = k^2/group_size; (t,h,w,k) the padded global grid.

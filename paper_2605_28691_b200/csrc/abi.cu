@@ -54,6 +54,34 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+int make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t cols, int64_t rows,
+                      int64_t row_stride_elems, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return kCuda;
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (row_stride_elems * 2) % 16 != 0) {
+    set_error("attention operands need 16-byte aligned base pointers and row strides");
+    return kValue;
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride_elems * 2)};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled (2d) failed (%d) cols=%lld rows=%lld",
+             static_cast<int>(r), static_cast<long long>(cols), static_cast<long long>(rows));
+    set_error(buf);
+    return kCuda;
+  }
+  return kOk;
+}
+
 int make_tmap_bf16_3d(CUtensorMap* map, const void* base, int64_t cols, int64_t rows,
                       int64_t n_seq, int64_t row_stride_elems, int box_rows) {
   EncodeTiledFn fn = encode_fn();
@@ -297,6 +325,49 @@ int osp_attn_bwd(const void* q, const void* k, const void* v, const void* o, con
   return launch_attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, s, q_stride, k_stride, v_stride,
                          o_stride, do_stride, dq_stride, dk_stride, dv_stride, valid_bits,
                          zero_invalid_queries, scale, workspace, workspace_bytes, as_stream(stream));
+}
+
+int osp_attn_fwd_gather(const void* q, const void* k, const void* v, void* o, float* lse,
+                        int64_t n_rows, const int32_t* row_index, const int32_t* seq_lens,
+                        int64_t n_seq, int64_t capacity, int64_t heads, int64_t head_dim,
+                        int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t o_stride,
+                        float scale, void* stream) {
+  int rc = attn_checks(n_seq, capacity, heads, head_dim);
+  if (rc != kOk) return rc;
+  if (!row_index || !seq_lens || n_rows <= 0 || capacity % 4) {
+    set_error("gather attention needs row_index, seq_lens, n_rows > 0 and capacity % 4 == 0");
+    return kValue;
+  }
+  if ((o_stride * 2) % 16 || (reinterpret_cast<uintptr_t>(o) & 15)) {
+    set_error("output needs 16-byte aligned base and row stride");
+    return kValue;
+  }
+  AttnShape s{n_seq, capacity, heads, head_dim, seq_lens, row_index, n_rows};
+  return launch_attn_fwd(q, k, v, o, lse, s, q_stride, k_stride, v_stride, o_stride, nullptr, 0,
+                         scale, as_stream(stream));
+}
+
+int osp_attn_bwd_gather(const void* q, const void* k, const void* v, const void* o,
+                        const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                        int64_t n_rows, const int32_t* row_index, const int32_t* seq_lens,
+                        int64_t n_seq, int64_t capacity, int64_t heads, int64_t head_dim,
+                        int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t o_stride,
+                        int64_t do_stride, int64_t dq_stride, int64_t dk_stride, int64_t dv_stride,
+                        float scale, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = attn_checks(n_seq, capacity, heads, head_dim);
+  if (rc != kOk) return rc;
+  if (!row_index || !seq_lens || n_rows <= 0 || capacity % 4) {
+    set_error("gather attention needs row_index, seq_lens, n_rows > 0 and capacity % 4 == 0");
+    return kValue;
+  }
+  AttnShape s{n_seq, capacity, heads, head_dim, seq_lens, row_index, n_rows};
+  if (workspace_bytes < attn_bwd_workspace_bytes(s)) {
+    set_error("attention backward workspace too small");
+    return kValue;
+  }
+  return launch_attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, s, q_stride, k_stride, v_stride,
+                         o_stride, do_stride, dq_stride, dk_stride, dv_stride, nullptr, 0, scale,
+                         workspace, workspace_bytes, as_stream(stream));
 }
 
 static int ssp_params(MapParams& p, int kind, int64_t group_size, int64_t local_batch, int64_t t,

@@ -51,6 +51,8 @@ struct BwdArgs {
   int words_per_seq;
   int seq_len, seq_pad, heads, n_q;  // seq_len = capacity (row stride of a sequence)
   const int* seq_lens;               // per-sequence valid length (<= seq_len) or null
+  const int* row_index;              // gather mode (D = 128): (n_seq, seq_len) token rows or -1
+  int n_rows;
   float scale, scale_log2;
   const __nv_bfloat16* k_rows;  // K (for the TMEM copy of the key tile)
   int64_t k_row_stride;
@@ -470,6 +472,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
   const int kv0 = blockIdx.x * 128;
   const int len = a.seq_lens ? __ldg(a.seq_lens + seq) : a.seq_len;
   if (kv0 >= len) {  // whole key tile past the sequence: dk, dv rows 0
+    if (a.row_index) return;  // gather mode: such rows have no destination
     const int r1 = min(kv0 + 128, a.seq_len);
     const int64_t hoff = static_cast<int64_t>(head) * D;
     zero_rows_bf16(a.dv + static_cast<int64_t>(seq) * a.seq_len * a.dv_stride + hoff, a.dv_stride, kv0, r1, D);
@@ -513,7 +516,50 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
   // register budget (setmaxnreg, total < 64K): control warps 56, compute 176, writers 88
   if (warp < 4) {
     regs_dec<56>();
-    if (warp == 0) {
+    if (warp == 0 && a.row_index) {
+      // -------------------------------------------------------------- TMA producer, gather mode:
+      // tile::gather4 of 4 token rows per lane and 64 columns (K, V once; Q, dO per query tile)
+      const int* ridx = a.row_index + static_cast<int64_t>(seq) * a.seq_len;
+      auto rows4 = [&](int row0) {
+        const int4 r = *reinterpret_cast<const int4*>(ridx + row0);
+        const int oob = a.n_rows;
+        return make_int4(r.x < 0 ? oob : r.x, r.y < 0 ? oob : r.y, r.z < 0 ? oob : r.z, r.w < 0 ? oob : r.w);
+      };
+      if (lane == 0) {
+        tma_prefetch(&tmQ);
+        tma_prefetch(&tmK);
+        tma_prefetch(&tmV);
+        tma_prefetch(&tmDO);
+        mbar_expect_tx(bar_kv, 65536);
+      }
+      __syncwarp();
+      {
+        const int4 r = rows4(kv0 + 4 * lane);
+        for (int s = 0; s < 2; ++s) {
+          tma_gather4(sm + Ly::kK + s * 16384 + lane * 512, &tmK, bar_kv, head * D + s * 64, r.x, r.y, r.z, r.w);
+          tma_gather4(sm + Ly::kV + s * 16384 + lane * 512, &tmV, bar_kv, head * D + s * 64, r.x, r.y, r.z, r.w);
+        }
+      }
+      const float* lse2_g = a.lse2 + sh * a.seq_pad;
+      const float* delta_g = a.delta + sh * a.seq_pad;
+      const int half_lane = lane & 15;  // lanes 0-15 fetch Q rows, 16-31 dO rows
+      const CUtensorMap* mapq = lane < 16 ? &tmQ : &tmDO;
+      const int base_off = lane < 16 ? Ly::kQ : Ly::kDO;
+      for (int i = 0; i < n_q; ++i) {
+        const int st = i % 3;
+        mbar_wait(bar_qe + st, ((i / 3) & 1) ^ 1);
+        if (lane == 0) {
+          mbar_expect_tx(bar_qf + st, 2 * 16384 + 512);
+          bulk_load(sm + Ly::kStat + st * 512, lse2_g + i * 64, 256, bar_qf + st);
+          bulk_load(sm + Ly::kStat + st * 512 + 256, delta_g + i * 64, 256, bar_qf + st);
+        }
+        __syncwarp();
+        const int4 r = rows4(i * 64 + 4 * half_lane);
+        for (int s = 0; s < 2; ++s)
+          tma_gather4(sm + base_off + st * 16384 + s * 8192 + half_lane * 512, mapq, bar_qf + st,
+                      head * D + s * 64, r.x, r.y, r.z, r.w);
+      }
+    } else if (warp == 0) {
       if (elect_one()) {
       // ---------------------------------------------------------------- TMA producer
       tma_prefetch(&tmQ);
@@ -649,8 +695,11 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       kvalid = (__ldg(vb + (kglob >> 5)) >> (kglob & 31)) & 1u;
     }
     if (half == 0)
-      row_to_tmem(tK + la, a.k_rows + (static_cast<int64_t>(seq) * a.seq_len + kglob) * a.k_row_stride +
-                               static_cast<int64_t>(head) * D, kglob < len);
+      row_to_tmem(tK + la,
+                  a.k_rows + (a.row_index ? (kglob < len ? static_cast<int64_t>(a.row_index[static_cast<int64_t>(seq) * a.seq_len + kglob]) : 0)
+                                          : static_cast<int64_t>(seq) * a.seq_len + kglob) * a.k_row_stride +
+                      static_cast<int64_t>(head) * D,
+                  kglob < len);
     tmem_wait_st();
     tc_fence_before();
     mbar_arrive(bar_kt);
@@ -745,15 +794,17 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
     // (warpgroup 0 drains dV, warpgroup 1 drains dK)
     mbar_wait(bar_fin, 0);
     tc_fence_after();
-    const bool row_ok = kglob < a.seq_len;  // rows in [len, cap) hold exact zeros
+    // rows in [len, cap) hold exact zeros; in gather mode they have no destination
+    const int64_t out_row =
+        a.row_index ? (kglob < len ? a.row_index[static_cast<int64_t>(seq) * a.seq_len + kglob] : -1)
+                    : (kglob < a.seq_len ? static_cast<int64_t>(seq) * a.seq_len + kglob : -1);
+    const bool row_ok = out_row >= 0;
     {
       const int which = half;
       const uint32_t base = (which == 0 ? tDV : tDK) + la;
       const float mul = which == 0 ? 1.f : a.scale;
-      __nv_bfloat16* dst =
-          (which == 0 ? a.dv : a.dk) +
-          (static_cast<int64_t>(seq) * a.seq_len + kglob) * (which == 0 ? a.dv_stride : a.dk_stride) +
-          static_cast<int64_t>(head) * D;
+      __nv_bfloat16* dst = (which == 0 ? a.dv : a.dk) + (row_ok ? out_row : 0) * (which == 0 ? a.dv_stride : a.dk_stride) +
+                           static_cast<int64_t>(head) * D;
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t o[32];
@@ -808,7 +859,8 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
 
 // dq = bf16(scale * acc) from the v2 (seq*head, q/4, d, q%4) accumulator.
 __global__ void dq_finalize_v2_kernel(const float* __restrict__ acc, __nv_bfloat16* dq, int64_t dq_stride,
-                                      int64_t n_seq, int heads, int seq_len, int seq_pad, float scale) {
+                                      int64_t n_seq, int heads, int seq_len, int seq_pad, float scale,
+                                      const int* __restrict__ row_index) {
   constexpr int D = 128;
   const int64_t nqb = seq_pad / 4;
   const int64_t total = n_seq * heads * nqb * D;
@@ -825,8 +877,10 @@ __global__ void dq_finalize_v2_kernel(const float* __restrict__ acc, __nv_bfloat
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t q = qb * 4 + j;
-      if (q < seq_len)
-        dq[(s * seq_len + q) * dq_stride + static_cast<int64_t>(h) * D + d] = __float2bfloat16(vv[j] * scale);
+      if (q < seq_len) {
+        const int64_t row = row_index ? row_index[s * seq_len + q] : s * seq_len + q;
+        if (row >= 0) dq[row * dq_stride + static_cast<int64_t>(h) * D + d] = __float2bfloat16(vv[j] * scale);
+      }
     }
   }
 }
@@ -836,7 +890,8 @@ template <int D>
 __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t o_stride,
                                 const __nv_bfloat16* __restrict__ dout, int64_t do_stride,
                                 const float* __restrict__ lse, float* lse2, float* delta, int64_t n_seq,
-                                int heads, int seq_len, int seq_pad, const int* __restrict__ seq_lens) {
+                                int heads, int seq_len, int seq_pad, const int* __restrict__ seq_lens,
+                                const int* __restrict__ row_index) {
   const int64_t total = n_seq * heads * static_cast<int64_t>(seq_pad);
   const int lane = threadIdx.x & 31;
   for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total;
@@ -848,8 +903,9 @@ __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t o_s
     const int len = seq_lens ? __ldg(seq_lens + s) : seq_len;
     float acc = 0.f;
     if (q < len) {
-      const __nv_bfloat16* orow = o + (s * seq_len + q) * o_stride + static_cast<int64_t>(h) * D;
-      const __nv_bfloat16* drow = dout + (s * seq_len + q) * do_stride + static_cast<int64_t>(h) * D;
+      const int64_t row = row_index ? row_index[s * seq_len + q] : s * seq_len + q;
+      const __nv_bfloat16* orow = o + row * o_stride + static_cast<int64_t>(h) * D;
+      const __nv_bfloat16* drow = dout + row * do_stride + static_cast<int64_t>(h) * D;
       for (int c = lane * 2; c < D; c += 64) {
         const float2 of = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(orow + c));
         const float2 df = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(drow + c));
@@ -921,17 +977,28 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     bwd_prep_kernel<D><<<grid_for(rows * 32, 256), 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(o), os, static_cast<const __nv_bfloat16*>(dout), dos, lse,
         w.lse2, w.delta, s.n_seq, static_cast<int>(s.heads), static_cast<int>(s.seq_len),
-        static_cast<int>(seq_pad), s.seq_lens);
+        static_cast<int>(seq_pad), s.seq_lens, s.row_index);
     rc = check_cuda(cudaGetLastError(), "bwd_prep launch");
     if (rc != kOk) return rc;
   }
   CUtensorMap mq, mk, mv, mdo;
   const int64_t cols = s.heads * D;
   const int qbox = D == 128 ? 64 : 128;
-  if ((rc = make_tmap_bf16_3d(&mq, q, cols, s.seq_len, s.n_seq, qs, qbox)) != kOk) return rc;
-  if ((rc = make_tmap_bf16_3d(&mk, k, cols, s.seq_len, s.n_seq, ks, 128)) != kOk) return rc;
-  if ((rc = make_tmap_bf16_3d(&mv, v, cols, s.seq_len, s.n_seq, vs, 128)) != kOk) return rc;
-  if ((rc = make_tmap_bf16_3d(&mdo, dout, cols, s.seq_len, s.n_seq, dos, qbox)) != kOk) return rc;
+  if (s.row_index) {
+    if (D != 128 || s.seq_len % 4) {
+      set_error("gather-mode backward needs head_dim 128 and a row-index capacity multiple of 4");
+      return kUnsupported;
+    }
+    if ((rc = make_tmap_bf16_2d(&mq, q, cols, s.n_rows, qs, 1)) != kOk) return rc;
+    if ((rc = make_tmap_bf16_2d(&mk, k, cols, s.n_rows, ks, 1)) != kOk) return rc;
+    if ((rc = make_tmap_bf16_2d(&mv, v, cols, s.n_rows, vs, 1)) != kOk) return rc;
+    if ((rc = make_tmap_bf16_2d(&mdo, dout, cols, s.n_rows, dos, 1)) != kOk) return rc;
+  } else {
+    if ((rc = make_tmap_bf16_3d(&mq, q, cols, s.seq_len, s.n_seq, qs, qbox)) != kOk) return rc;
+    if ((rc = make_tmap_bf16_3d(&mk, k, cols, s.seq_len, s.n_seq, ks, 128)) != kOk) return rc;
+    if ((rc = make_tmap_bf16_3d(&mv, v, cols, s.seq_len, s.n_seq, vs, 128)) != kOk) return rc;
+    if ((rc = make_tmap_bf16_3d(&mdo, dout, cols, s.seq_len, s.n_seq, dos, qbox)) != kOk) return rc;
+  }
   if ((dks * 2) % 16 || (dvs * 2) % 16 || (reinterpret_cast<uintptr_t>(dk) & 15) ||
       (reinterpret_cast<uintptr_t>(dv) & 15) || (dqs * 2) % 8 || (reinterpret_cast<uintptr_t>(dq) & 7)) {
     set_error("gradient outputs need 16-byte aligned bases/row strides");
@@ -949,6 +1016,8 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
   a.words_per_seq = static_cast<int>((s.seq_len + 31) / 32);
   a.seq_len = static_cast<int>(s.seq_len);
   a.seq_lens = s.seq_lens;
+  a.row_index = s.row_index;
+  a.n_rows = static_cast<int>(s.n_rows);
   a.seq_pad = static_cast<int>(seq_pad);
   a.heads = static_cast<int>(s.heads);
   a.n_q = static_cast<int>(seq_pad / 128);
@@ -980,7 +1049,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     if (rc != kOk) return rc;
     dq_finalize_v2_kernel<<<grid_for(s.n_seq * s.heads * seq_pad / 4 * D, 256), 256, 0, stream>>>(
         w.dq_acc, static_cast<__nv_bfloat16*>(dq), dqs, s.n_seq, static_cast<int>(s.heads),
-        static_cast<int>(s.seq_len), static_cast<int>(seq_pad), scale);
+        static_cast<int>(s.seq_len), static_cast<int>(seq_pad), scale, s.row_index);
     return check_cuda(cudaGetLastError(), "dq_finalize_v2 launch");
   }
   attn_bwd_kernel<D><<<grid, kBwdThreads, BwdLayout<D>::kSmem, stream>>>(mq, mk, mv, mdo, a);

@@ -49,6 +49,8 @@ struct FwdArgs {
   int words_per_seq;
   int seq_len;              // capacity (row stride of a sequence)
   const int* seq_lens;      // per-sequence valid length (<= seq_len) or null
+  const int* row_index;     // gather mode: (n_seq, seq_len) token rows of q/k/v/o (-1 = none)
+  int n_rows;               // gather mode: rows of the q/k/v/o tensors
   int heads;
   float scale_log2;
   int zero_invalid_q;
@@ -89,8 +91,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int len = a.seq_lens ? __ldg(a.seq_lens + seq) : a.seq_len;
   if (q_row0 >= len) {  // whole CTA past the sequence: o rows 0, lse +inf
     const int r1 = min(q_row0 + 2 * kBM, a.seq_len);
-    zero_rows_bf16(a.o + static_cast<int64_t>(seq) * a.seq_len * a.o_stride + static_cast<int64_t>(head) * D,
-                   a.o_stride, q_row0, r1, D);
+    if (!a.row_index)  // gather mode: rows past the length have no destination
+      zero_rows_bf16(a.o + static_cast<int64_t>(seq) * a.seq_len * a.o_stride + static_cast<int64_t>(head) * D,
+                     a.o_stride, q_row0, r1, D);
     for (int r = q_row0 + static_cast<int>(threadIdx.x); r < r1; r += blockDim.x)
       a.lse[(static_cast<int64_t>(seq) * a.heads + head) * a.seq_len + r] = INFINITY;
     return;
@@ -121,7 +124,41 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   if (warp < 4) {
     regs_dec<56>();
-  if (warp == 0) {
+  if (warp == 0 && a.row_index) {
+    // -------------------------------------------------------------- TMA producer, gather mode:
+    // each lane fetches 4 token rows of a 128-row tile with one tile::gather4 per 64 columns
+    const int* ridx = a.row_index + static_cast<int64_t>(seq) * a.seq_len;
+    auto gather_tile = [&](uint8_t* dst, const CUtensorMap* m, uint64_t* bar, int row0) {
+      const int4 r = *reinterpret_cast<const int4*>(ridx + row0 + 4 * lane);
+      const int oob = a.n_rows;  // out-of-range rows are zero-filled by the TMA
+      const int r0 = r.x < 0 ? oob : r.x, r1 = r.y < 0 ? oob : r.y, r2 = r.z < 0 ? oob : r.z,
+                r3 = r.w < 0 ? oob : r.w;
+#pragma unroll
+      for (int s = 0; s < Ly::kSub; ++s)
+        tma_gather4(dst + s * 16384 + lane * 512, m, bar, head * D + s * 64, r0, r1, r2, r3);
+    };
+    if (lane == 0) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      mbar_expect_tx(bar_q + 0, Ly::kTile);
+      mbar_expect_tx(bar_q + 1, Ly::kTile);
+    }
+    __syncwarp();
+    for (int t = 0; t < 2; ++t) gather_tile(sm + Ly::kQ + t * Ly::kTile, &tmQ, bar_q + t, q_row0 + t * kBM);
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j & 1;
+      const uint32_t ph = (j >> 1) & 1;
+      mbar_wait(bar_ke + st, ph ^ 1);
+      if (lane == 0) mbar_expect_tx(bar_kf + st, Ly::kTile);
+      __syncwarp();
+      gather_tile(sm + Ly::kK + st * Ly::kTile, &tmK, bar_kf + st, j * kBN);
+      mbar_wait(bar_ve + st, ph ^ 1);
+      if (lane == 0) mbar_expect_tx(bar_vf + st, Ly::kTile);
+      __syncwarp();
+      gather_tile(sm + Ly::kV + st * Ly::kTile, &tmV, bar_vf + st, j * kBN);
+    }
+  } else if (warp == 0) {
     if (elect_one()) {
       // ------------------------------------------------------------ TMA producer
       tma_prefetch(&tmQ);
@@ -369,14 +406,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (a.zero_invalid_q && vbits && row_ok) q_valid = bit_at(vbits, a.words_per_seq, q_row);
     const bool live = row_ok && q_valid && l > 0.f;
     const float inv_l = live ? 1.f / l : 0.f;
-    __nv_bfloat16* orow = a.o + (static_cast<int64_t>(seq) * a.seq_len + q_row) * a.o_stride +
-                          static_cast<int64_t>(head) * D;
+    const int64_t out_row =
+        a.row_index ? (row_ok ? a.row_index[static_cast<int64_t>(seq) * a.seq_len + q_row] : -1)
+                    : static_cast<int64_t>(seq) * a.seq_len + q_row;
+    const bool write_o = a.row_index ? out_row >= 0 : in_cap;
+    __nv_bfloat16* orow = a.o + out_row * a.o_stride + static_cast<int64_t>(head) * D;
 #pragma unroll
     for (int cc = 0; cc < D / 32; ++cc) {
       uint32_t o[32];
       tmem_ld32(tO + cc * 32, o);
       tmem_wait_ld(o);
-      if (in_cap) {
+      if (write_o) {
         uint4 pk[4];
         uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
 #pragma unroll
@@ -409,9 +449,19 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
   CUtensorMap mq, mk, mv;
   const int64_t cols = s.heads * D;
   int st;
-  if ((st = make_tmap_bf16_3d(&mq, q, cols, s.seq_len, s.n_seq, qs, kBM)) != kOk) return st;
-  if ((st = make_tmap_bf16_3d(&mk, k, cols, s.seq_len, s.n_seq, ks, kBN)) != kOk) return st;
-  if ((st = make_tmap_bf16_3d(&mv, v, cols, s.seq_len, s.n_seq, vs, kBN)) != kOk) return st;
+  if (s.row_index) {
+    if (s.seq_len % 4) {
+      set_error("gather mode needs the row-index capacity to be a multiple of 4");
+      return kValue;
+    }
+    if ((st = make_tmap_bf16_2d(&mq, q, cols, s.n_rows, qs, 1)) != kOk) return st;
+    if ((st = make_tmap_bf16_2d(&mk, k, cols, s.n_rows, ks, 1)) != kOk) return st;
+    if ((st = make_tmap_bf16_2d(&mv, v, cols, s.n_rows, vs, 1)) != kOk) return st;
+  } else {
+    if ((st = make_tmap_bf16_3d(&mq, q, cols, s.seq_len, s.n_seq, qs, kBM)) != kOk) return st;
+    if ((st = make_tmap_bf16_3d(&mk, k, cols, s.seq_len, s.n_seq, ks, kBN)) != kOk) return st;
+    if ((st = make_tmap_bf16_3d(&mv, v, cols, s.seq_len, s.n_seq, vs, kBN)) != kOk) return st;
+  }
   FwdArgs a;
   a.o = static_cast<__nv_bfloat16*>(o);
   a.o_stride = os;
@@ -421,6 +471,8 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
   a.seq_len = static_cast<int>(s.seq_len);
   a.heads = static_cast<int>(s.heads);
   a.seq_lens = s.seq_lens;
+  a.row_index = s.row_index;
+  a.n_rows = static_cast<int>(s.n_rows);
   a.scale_log2 = scale * 1.4426950408889634f;
   a.zero_invalid_q = zero_invalid_q;
   {

@@ -75,6 +75,18 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uin
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// Four arbitrary rows (2-D tensor map, box {64 cols, 1 row}) into 4 consecutive 128-byte smem
+// rows; rows >= the tensor extent are zero-filled.  With 128B swizzle the image equals a tile
+// load of the same rows (measured, tools/tma_gather_probe.cu).
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* m, uint64_t* bar, int col,
+                                            int r0, int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
 // Same box delivered to the same smem offset (and mbarrier offset) of every CTA in cta_mask.
 __device__ __forceinline__ void tma_load_3d_multicast(void* dst, const CUtensorMap* m, uint64_t* bar,
                                                       int c0, int c1, int c2, uint16_t cta_mask) {

@@ -33,6 +33,11 @@ int check_cuda(cudaError_t e, const char* what);
 int make_tmap_bf16_3d(CUtensorMap* map, const void* base, int64_t cols, int64_t rows,
                       int64_t n_seq, int64_t row_stride_elems, int box_rows);
 
+// 2-D bf16 TMA descriptor over a (rows, cols) row-strided matrix with a (64 x box_rows) box and
+// 128-byte swizzle (box_rows = 1 for tile::gather4 row gathers).
+int make_tmap_bf16_2d(CUtensorMap* map, const void* base, int64_t cols, int64_t rows,
+                      int64_t row_stride_elems, int box_rows);
+
 // Closed-form row map of the rearrange engine (rearrange.cu).
 struct MapParams {
   int kind;
@@ -47,6 +52,10 @@ struct MapParams {
 struct AttnShape {
   int64_t n_seq, seq_len, heads, head_dim;  // seq_len = capacity (row stride of a sequence)
   const int32_t* seq_lens = nullptr;         // optional per-sequence valid lengths (<= seq_len)
+  // gather mode: q/k/v/o/dO/dq/dk/dv are (n_rows, >= heads*head_dim) tensors in any token
+  // layout; row j of sequence s is row row_index[s * seq_len + j] (-1 = none)
+  const int32_t* row_index = nullptr;
+  int64_t n_rows = 0;
 };
 
 int launch_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,

@@ -222,6 +222,54 @@ def attn_bwd(q, k, v, o, do, lse, heads: int, head_dim: int, valid_bits, zero_in
     return dq, dk, dv
 
 
+def attn_fwd_gather(q, k, v, heads: int, head_dim: int, row_index: torch.Tensor,
+                    seq_lens: torch.Tensor, scale: float, out: torch.Tensor | None = None):
+    """Gather-mode attention: q, k, v (n_rows, >= C) in any token layout; subsequence s is rows
+    row_index[s, :seq_lens[s]] ((n_seq, capacity) int32, -1 padded).  Returns (o (n_rows, C)
+    with only the indexed rows written, lse (n_seq, heads, capacity))."""
+    L = _lib.lib()
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        _cuda(t, name)
+        if t.dtype != torch.bfloat16 or t.stride(-1) != 1:
+            raise UnsupportedError(f"{name} must be bf16 with unit column stride")
+    n_rows = q.shape[0]
+    n_seq, cap = row_index.shape
+    if out is None:
+        out = torch.empty((n_rows, heads * head_dim), dtype=torch.bfloat16, device=q.device)
+    lse = torch.empty((n_seq, heads, cap), dtype=torch.float32, device=q.device)
+    ri = row_index.to(torch.int32).contiguous()
+    sl = _lens(seq_lens, n_seq, cap)
+    _lib.check(STATS.run('attn_fwd', 1, lambda: L.osp_attn_fwd_gather(
+        q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr(), n_rows, ri.data_ptr(),
+        sl.data_ptr(), n_seq, cap, heads, head_dim, q.stride(0), k.stride(0), v.stride(0), out.stride(0),
+        float(scale), _lib.stream_ptr(q.device))))
+    return out, lse
+
+
+def attn_bwd_gather(q, k, v, o, do, lse, heads: int, head_dim: int, row_index, seq_lens, scale: float,
+                    dq=None, dk=None, dv=None):
+    L = _lib.lib()
+    n_rows = q.shape[0]
+    n_seq, cap = row_index.shape
+    C = heads * head_dim
+    dev = q.device
+    if do.stride(-1) != 1:
+        do = do.contiguous()
+    dq = dq if dq is not None else torch.empty((n_rows, C), dtype=torch.bfloat16, device=dev)
+    dk = dk if dk is not None else torch.empty((n_rows, C), dtype=torch.bfloat16, device=dev)
+    dv = dv if dv is not None else torch.empty((n_rows, C), dtype=torch.bfloat16, device=dev)
+    ws_bytes = L.osp_attn_bwd_workspace_bytes(n_seq, cap, heads, head_dim)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    ri = row_index.to(torch.int32).contiguous()
+    sl = _lens(seq_lens, n_seq, cap)
+    _lib.check(STATS.run('attn_bwd', 3, lambda: L.osp_attn_bwd_gather(
+        q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(),
+        dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), n_rows, ri.data_ptr(), sl.data_ptr(), n_seq, cap,
+        heads, head_dim, q.stride(0), k.stride(0), v.stride(0), o.stride(0), do.stride(0), dq.stride(0),
+        dk.stride(0), dv.stride(0), float(scale), ws.data_ptr(), ws_bytes, _lib.stream_ptr(dev))))
+    return dq, dk, dv
+
+
 def ssp_pack(x: torch.Tensor, group_size: int, t: int, h: int, w: int, k: int) -> torch.Tensor:
     L = _lib.lib()
     _cuda(x, "x")

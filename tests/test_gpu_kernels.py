@@ -239,3 +239,55 @@ def test_attention_varlen_matches_per_sequence_runs(lib, lens, heads, d):
     for t in (o, dq, dk, dv):                  # rows beyond a sequence's length are zero
         assert (t.cpu()[~valid] == 0).all()
     assert torch.isinf(lse.cpu().transpose(1, 2)[~valid]).all()
+
+
+@pytest.mark.parametrize("lens,heads", [((1000, 777, 0, 130), 2), ((2048, 1999), 1)])
+def test_attention_gather_mode_matches_reference(lib, lens, heads):
+    """Gather mode (rearrange fused into the TMA prologue / epilogue): q/k/v/o and the gradients
+    live in an arbitrary token order; subsequence s is rows row_index[s, :len_s]."""
+    from paper_2605_28691_b200 import kernels
+    d = 128
+    C = heads * d
+    n_seq = len(lens)
+    cap = (max(lens) + 127) // 128 * 128
+    n_rows = sum(lens) + 50                       # some rows belong to no subsequence
+    rng = np.random.default_rng(sum(lens) + 1)
+    perm = rng.permutation(n_rows)
+    ri = -np.ones((n_seq, cap), dtype=np.int32)
+    off = 0
+    for s, L in enumerate(lens):
+        ri[s, :L] = perm[off:off + L]
+        off += L
+    qkv = _bf16(rng.standard_normal((n_rows, 3 * C)))
+    do = _bf16(rng.standard_normal((n_rows, C)))
+    dev_qkv = qkv.to(_dev())
+    q, k, v = dev_qkv[:, :C], dev_qkv[:, C:2 * C], dev_qkv[:, 2 * C:]
+    ridx = torch.from_numpy(ri).to(_dev())
+    sl = torch.tensor(lens, dtype=torch.int32, device=_dev())
+    sentinel = torch.full((n_rows, C), 7.0, dtype=torch.bfloat16, device=_dev())
+    o, lse = kernels.attn_fwd_gather(q, k, v, heads, d, ridx, sl, 1 / math.sqrt(d), out=sentinel.clone())
+    dq, dk, dv = kernels.attn_bwd_gather(q, k, v, o, do.to(_dev()), lse, heads, d, ridx, sl,
+                                         1 / math.sqrt(d), dq=sentinel.clone(), dk=sentinel.clone(),
+                                         dv=sentinel.clone())
+    used = np.zeros(n_rows, dtype=bool)
+    for s, L in enumerate(lens):
+        if L == 0:
+            continue
+        rows = torch.from_numpy(ri[s, :L].astype(np.int64))
+        used[ri[s, :L]] = True
+        leaves = [qkv[rows][None, :, i * C:(i + 1) * C].double().requires_grad_() for i in range(3)]
+        ref = attention_ref(*leaves, heads)
+        ref.backward(do[rows][None].double())
+        lp = [qkv[rows][None, :, i * C:(i + 1) * C].clone().requires_grad_() for i in range(3)]
+        pt = attention_ref(*lp, heads, upcast=False)
+        pt.backward(do[rows][None])
+        e = (o.cpu()[rows].double() - ref.detach()[0]).abs().max().item()
+        e_pt = (pt.detach()[0].double() - ref.detach()[0]).abs().max().item()
+        assert e <= 2 * e_pt + 1e-3, ("fwd", s, e, e_pt)
+        for name, got, r, p in zip("qkv", (dq, dk, dv), leaves, lp):
+            e = (got.cpu()[rows].double() - r.grad[0]).abs().max().item()
+            e_pt = (p.grad[0].double() - r.grad[0]).abs().max().item()
+            assert e <= 2 * e_pt + 2e-3, (name, s, e, e_pt)
+    unused = torch.from_numpy(~used)
+    for t in (o, dq, dk, dv):                     # rows outside every subsequence are untouched
+        assert (t.cpu()[unused] == 7.0).all()
