@@ -264,7 +264,7 @@ def run_ours(args, world, rank, local_rank):
     # ---- end-to-end through the public API (pinned host input, loss read back).  Every step's
     # input is copied host->device inside the timed region; the copy of step i+1 runs on a
     # copy stream (double buffer) while step i computes, as a training loop's data feed would.
-    host_x = torch.empty((blk.local_rows, blk.L, C), dtype=torch.bfloat16, pin_memory=True)
+    host_x = torch.empty(tuple(x.shape), dtype=torch.bfloat16, pin_memory=True)
     host_x.copy_(x.detach().cpu())
     host_loss = torch.empty((args.steps,), dtype=torch.float32, pin_memory=True)
     bufs = [torch.empty_like(x.detach()) for _ in range(2)]

@@ -21,7 +21,7 @@ import torch.nn.functional as F
 
 from . import kernels
 from .anyres import PaddedGrid
-from .errors import ShapeError
+from .errors import ShapeError, UnsupportedError
 from .gridseq import GridShape, SequenceTensor, default_device
 from .skiparse import SparsePattern, assignment_of, inverse_pattern_map, pattern_map
 
@@ -107,6 +107,46 @@ class _Attn(torch.autograd.Function):
         dq, dk, dv = kernels.attn_bwd(q, k, v, o, do.contiguous(), lse, heads, d, bits, zero_q,
                                       scale, seq_lens=seq_lens)
         return dq, dk, dv, None, None, None, None, None, None
+
+
+class _AttnGather(torch.autograd.Function):
+    """Fused-rearrange attention over a token-major packed (n_rows, 3*C) [q | k | v]: the
+    subsequences of a pattern are read and written through a GatherPlan row table (K2/K3
+    gather mode); the result is token-major too."""
+
+    @staticmethod
+    def forward(ctx, qkv, heads, d, plan, scale):
+        C = heads * d
+        q, k, v = qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:]
+        out = None if plan.covers_all else torch.zeros((qkv.shape[0], C), dtype=qkv.dtype, device=qkv.device)
+        o, lse = kernels.attn_fwd_gather(q, k, v, heads, d, plan.row_index, plan.lens, scale, out=out)
+        ctx.save_for_backward(qkv, o, lse)
+        ctx.cfg = (heads, d, plan, scale)
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        qkv, o, lse = ctx.saved_tensors
+        heads, d, plan, scale = ctx.cfg
+        C = heads * d
+        dqkv = torch.empty_like(qkv) if plan.covers_all else torch.zeros_like(qkv)
+        kernels.attn_bwd_gather(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], o, do.contiguous(), lse,
+                                heads, d, plan.row_index, plan.lens, scale, dq=dqkv[:, :C],
+                                dk=dqkv[:, C:2 * C], dv=dqkv[:, 2 * C:])
+        return dqkv, None, None, None, None
+
+
+def attention_gather(qkv: torch.Tensor, heads: int, plan, scale: float | None = None) -> torch.Tensor:
+    """Skiparse attention with the rearrange fused into the kernels' TMA loads / stores:
+    qkv (..., n_rows, 3*C) token-major bf16, plan = compact.GatherPlan.  head_dim 128."""
+    shape = qkv.shape
+    C = shape[-1] // 3
+    d = C // heads
+    if d != 128:
+        raise UnsupportedError("gather-mode attention runs head_dim 128")
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    o = _AttnGather.apply(qkv.reshape(-1, 3 * C).contiguous(), heads, d, plan, scale)
+    return o.view(*shape[:-1], C)
 
 
 def _pad_heads(t: torch.Tensor, heads: int, d: int, dp: int) -> torch.Tensor:

@@ -89,6 +89,13 @@ class SkiparseBlock:
         self.plan_gsa = self.pg.compact_plan(SparsePattern.GROUP_WISE, batch, (r0, r1)) if compact else None
         self._t2g = IndexMap._pattern("tsa_to_gsa", self.grid, batch)
         self._g2t = IndexMap._pattern("gsa_to_tsa", self.grid, batch)
+        # one GPU, head_dim 128: the rearranges are fused into the attention kernels' TMA loads and
+        # stores (gather mode) -- activations stay in the original latent layout end to end
+        self.gather = None
+        if self.world == 1 and chan // heads == 128:
+            from .compact import gather_plan
+            self.gather = (gather_plan(g, SparsePattern.TOKEN_WISE, batch, self.pg, "original"),
+                           gather_plan(g, SparsePattern.GROUP_WISE, batch, self.pg, "original"))
         # one GPU with compaction: fold expand -> pattern switch -> compact into one row move
         # each way (compact TSA -> compact GSA, compact GSA -> padded TSA)
         self._fused = None
@@ -133,6 +140,23 @@ class SkiparseBlock:
         if plan is not None:
             return expand_rows(attention_packed(qkv, self.heads, seq_lens=plan.lens), plan)
         return attention_packed(qkv, self.heads, bits, zero_invalid_queries=bits is not None)
+
+    def forward_original(self, x: torch.Tensor) -> torch.Tensor:
+        """One GPU: the block on the original (unpadded) latent layout (B, T*H0*W0, C) -- TSA
+        application then GSA application with no rearranged copy in HBM (gather-mode kernels)."""
+        if self.gather is None:
+            raise ValueError("forward_original needs one GPU and head_dim 128")
+        from .attention import attention_gather
+        for W, Wt, plan, pat in ((self.W1, getattr(self, "W1t", None), self.gather[0], SparsePattern.TOKEN_WISE),
+                                 (self.W2, getattr(self, "W2t", None), self.gather[1], SparsePattern.GROUP_WISE)):
+            if self.prologue:
+                from .prologue import QKVPrologue
+                qkv = QKVPrologue.apply(x, self.g, SparsePattern.ORIGINAL, self.batch, self.qk_norm,
+                                        self.gamma_q, self.gamma_k, self.eps, self.rope, 0, Wt)
+            else:
+                qkv = torch.matmul(x, W)
+            x = attention_gather(qkv, self.heads, plan)
+        return x
 
     def _call_fused(self, x_tsa):
         from .compact import apply_move, compact_rows

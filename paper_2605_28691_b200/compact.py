@@ -18,7 +18,8 @@ import torch
 
 from . import kernels
 
-__all__ = ["CompactPlan", "compact_plan", "compact_rows", "expand_rows", "RowMove", "row_move"]
+__all__ = ["CompactPlan", "compact_plan", "compact_rows", "expand_rows", "RowMove", "row_move",
+           "GatherPlan", "gather_plan"]
 
 
 @dataclass(frozen=True)
@@ -124,3 +125,60 @@ class _Move(torch.autograd.Function):
 
 def apply_move(x: torch.Tensor, mv: RowMove) -> torch.Tensor:
     return _Move.apply(x, mv)
+
+
+@dataclass(frozen=True)
+class GatherPlan:
+    """Row table of the fused-rearrange attention (gather mode, K2/K3): subsequence s of a
+    pattern is rows row_index[s, :lens[s]] of a token-major tensor (the original latent layout),
+    so no rearranged copy is ever materialised."""
+
+    row_index: torch.Tensor   # (n_seq, cap) int32, -1 beyond lens[s]; cap % 128 == 0
+    lens: torch.Tensor        # (n_seq,) int32
+    n_rows: int               # rows of the token-major tensors
+    covers_all: bool          # every row belongs to some subsequence
+
+
+def gather_plan(grid, pattern, batch: int = 1, pg=None, target: str = "original",
+                rows: tuple | None = None) -> GatherPlan:
+    """Table for `pattern` subsequences [rows) of `batch` items on the padded grid of `pg`
+    (or `grid` when unpadded).  target "original": rows of the unpadded (batch, T*H0*W0) latent
+    (pad tokens simply never appear); "padded": rows of the padded (batch, T*H*W) latent."""
+    from .skiparse import SparsePattern, pattern_map
+    from .gridseq import default_device
+    padded = pg.padded if pg is not None else grid
+    dev = default_device()
+    S = padded.seq_len
+    pat = SparsePattern(pattern)
+    k2 = 1 if pat is SparsePattern.ORIGINAL else padded.k * padded.k
+    L = S // k2
+    if pat is SparsePattern.ORIGINAL:
+        src = torch.arange(batch * S, device=dev, dtype=torch.int64).view(batch, S)
+    else:
+        src = pattern_map(padded, pat, batch).src.to(dev).view(batch * k2, L)   # -> b*S + token
+    if pg is not None and not pg.trivial:
+        mask = pg.mask.to(dev).bool()                                  # (S,) real tokens
+        valid = mask[src % S]
+    else:
+        valid = torch.ones_like(src, dtype=torch.bool)
+    if rows is not None:
+        src, valid = src[rows[0]:rows[1]], valid[rows[0]:rows[1]]
+    if target == "original" and pg is not None and not pg.trivial:
+        real_idx = torch.cumsum(mask.to(torch.int64), 0) - 1          # padded token -> real index
+        S_real = int(mask.sum())
+        dest = (src // S) * S_real + real_idx[src % S]
+        n_rows = batch * S_real
+    else:
+        dest = src
+        n_rows = batch * S
+    n_seq = src.shape[0]
+    lens = valid.sum(dim=1)
+    cap = max(int(lens.max().item()) if n_seq else 0, 1)
+    cap = (cap + 127) // 128 * 128
+    j = torch.cumsum(valid.to(torch.int64), dim=1) - 1
+    table = torch.full((n_seq, cap), -1, dtype=torch.int64, device=dev)
+    srow = torch.arange(n_seq, device=dev)[:, None].expand_as(j)
+    table[srow[valid], j[valid]] = dest[valid]
+    covered = int(lens.sum()) == n_rows
+    return GatherPlan(table.to(torch.int32).contiguous(), lens.to(torch.int32).contiguous(), n_rows,
+                      covered)

@@ -348,3 +348,41 @@ def test_block_compaction_paths_agree_fwd_bwd(P):
     assert (ga[~real] == 0).all()
     rel = (ga - gb).abs().max().item() / gb.abs().max().item()
     assert rel < 2e-2, rel
+
+
+@pytest.mark.parametrize("grid", [(2, 10, 12, 2), (2, 8, 16, 2)])
+def test_block_forward_original_matches_pattern_layout_block(P, grid):
+    """Gather-mode block (rearranges fused into the attention kernels, original unpadded layout)
+    equals the pattern-layout block composed with explicit rearranges, fwd and input grad."""
+    from paper_2605_28691_b200.block import SkiparseBlock
+    g = P.GridShape(*grid)
+    pg = P.pad_grid(g)
+    C, heads = 256, 2
+    blk = SkiparseBlock(g, heads, C)
+    assert blk.gather is not None
+    torch.manual_seed(4)
+    x = torch.randn(1, g.seq_len, C, device="cuda").to(torch.bfloat16)
+    xa = x.clone().requires_grad_(True)
+    ya = blk.forward_original(xa)
+    xt = blk.to_local_tsa(x).detach().requires_grad_(True)
+    yt = blk(xt)
+    p = pg.padded
+    yb = P.kernels.rearrange(yt.detach(), "tsa_to_orig", p.t, p.h, p.w, p.k, 1, g.h, g.w)
+    assert (ya.float() - yb.float()).abs().max().item() < 2e-2
+    gy = torch.randn_like(ya)
+    ya.backward(gy)
+    # the maps are permutations with zero pad rows: push gy into the TSA layout, pull back
+    yt.backward(P.kernels.rearrange(gy, "orig_to_tsa", p.t, p.h, p.w, p.k, 1, g.h, g.w))
+    gb = P.kernels.rearrange(xt.grad, "tsa_to_orig", p.t, p.h, p.w, p.k, 1, g.h, g.w)
+    rel = (xa.grad.float() - gb.float()).abs().max().item() / gb.float().abs().max().item()
+    assert rel < 2e-2, rel
+
+
+def test_block_forward_original_with_prologue(P):
+    from paper_2605_28691_b200.block import SkiparseBlock
+    g = P.GridShape(2, 10, 12, 2)
+    blk = SkiparseBlock(g, 2, 256, qk_norm="head", rope=True)
+    x = torch.randn(1, g.seq_len, 256, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    y = blk.forward_original(x)
+    y.float().sum().backward()
+    assert torch.isfinite(y).all() and torch.isfinite(x.grad).all()
