@@ -5,7 +5,6 @@ Host I/O only: device tensors are copied to the host to be written."""
 from __future__ import annotations
 
 import struct
-from pathlib import Path
 
 import numpy as np
 import torch

@@ -86,7 +86,6 @@ def qkv_project(x: torch.Tensor, grid: GridShape, pattern: SparsePattern = Spars
 
 def _rope_cos_sin(grid: GridShape, pattern, batch: int, rows: int, row_offset: int, device, theta):
     """(rows, 64) cos / sin of every pair's angle (backward only)."""
-    from .skiparse import assignment_of
     pat = SparsePattern(pattern)
     if pat is SparsePattern.ORIGINAL:
         flat = torch.arange(grid.seq_len, device=device)
