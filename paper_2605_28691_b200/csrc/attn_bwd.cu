@@ -885,36 +885,46 @@ __global__ void dq_finalize_v2_kernel(const float* __restrict__ acc, __nv_bfloat
   }
 }
 
-// delta and log2-domain lse per (seq, head, query), padded to seq_pad; one warp per row.
+// delta and log2-domain lse per (seq, head, query), padded to seq_pad.  D/8 lanes per row, each
+// with one 16-byte load of O and of dO (a row's head slice is one contiguous 2*D-byte segment).
 template <int D>
 __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t o_stride,
                                 const __nv_bfloat16* __restrict__ dout, int64_t do_stride,
                                 const float* __restrict__ lse, float* lse2, float* delta, int64_t n_seq,
                                 int heads, int seq_len, int seq_pad, const int* __restrict__ seq_lens,
                                 const int* __restrict__ row_index) {
+  constexpr int G = D / 8;             // lanes per row
+  constexpr int R = 32 / G;            // rows per warp
   const int64_t total = n_seq * heads * static_cast<int64_t>(seq_pad);
   const int lane = threadIdx.x & 31;
-  for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < total;
-       w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
-    const int q = static_cast<int>(w % seq_pad);
-    const int64_t sh = w / seq_pad;
+  const int sub = lane / G, gl = lane % G;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t wb = warp0 * R; wb < total; wb += nwarps * R) {
+    const int64_t w = wb + sub;
+    const bool in = w < total;
+    const int q = in ? static_cast<int>(w % seq_pad) : 0;
+    const int64_t sh = in ? w / seq_pad : 0;
     const int h = static_cast<int>(sh % heads);
     const int64_t s = sh / heads;
     const int len = seq_lens ? __ldg(seq_lens + s) : seq_len;
     float acc = 0.f;
-    if (q < len) {
+    if (in && q < len) {
       const int64_t row = row_index ? row_index[s * seq_len + q] : s * seq_len + q;
-      const __nv_bfloat16* orow = o + row * o_stride + static_cast<int64_t>(h) * D;
-      const __nv_bfloat16* drow = dout + row * do_stride + static_cast<int64_t>(h) * D;
-      for (int c = lane * 2; c < D; c += 64) {
-        const float2 of = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(orow + c));
-        const float2 df = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(drow + c));
+      const uint4 ov = *reinterpret_cast<const uint4*>(o + row * o_stride + static_cast<int64_t>(h) * D + gl * 8);
+      const uint4 dv = *reinterpret_cast<const uint4*>(dout + row * do_stride + static_cast<int64_t>(h) * D + gl * 8);
+      const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+      const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 of = __bfloat1622float2(o2[j]);
+        const float2 df = __bfloat1622float2(d2[j]);
         acc += of.x * df.x + of.y * df.y;
       }
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, off);
-    if (lane == 0) {
+    for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, off);
+    if (in && gl == 0) {
       delta[w] = acc;
       lse2[w] = q < len ? lse[sh * seq_len + q] * kLog2e : INFINITY;
     }
@@ -969,12 +979,16 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
                  int64_t dvs, const uint32_t* bits, float scale, void* workspace, cudaStream_t stream) {
   const int64_t seq_pad = (s.seq_len + 127) / 128 * 128;
   BwdWs w = carve(workspace, s);
+  if ((os % 8) || (dos % 8) || (reinterpret_cast<uintptr_t>(o) & 15) || (reinterpret_cast<uintptr_t>(dout) & 15)) {
+    set_error("o / dout need 16-byte aligned bases and row strides");
+    return kValue;
+  }
   int rc = check_cuda(cudaMemsetAsync(w.dq_acc, 0, s.n_seq * seq_pad * s.heads * D * 4, stream),
                       "memset dq_acc");
   if (rc != kOk) return rc;
   {
     const int64_t rows = s.n_seq * s.heads * seq_pad;
-    bwd_prep_kernel<D><<<grid_for(rows * 32, 256), 256, 0, stream>>>(
+    bwd_prep_kernel<D><<<grid_for(rows * 32 / (32 / (D / 8)), 256), 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(o), os, static_cast<const __nv_bfloat16*>(dout), dos, lse,
         w.lse2, w.delta, s.n_seq, static_cast<int>(s.heads), static_cast<int>(s.seq_len),
         static_cast<int>(seq_pad), s.seq_lens, s.row_index);
