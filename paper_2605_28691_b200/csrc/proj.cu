@@ -15,22 +15,24 @@
 //                          form from its pattern-layout row (skiparse.py:68-114 inverted).
 // The reference's projection (attention.py:20-32) is this GEMM with norm 0 and rope off.
 //
-// Kernel: persistent, clusters of two CTAs (one per SM) on vertically adjacent 128 x 256 output
-// tiles that share their 256 x 64 weight slice per K step: each CTA loads its own x rows and
-// half of the weight slice, TMA-multicast into both CTAs (half the L2 -> SM traffic of W; the
-// shape cuBLAS uses for this GEMM).  64-deep K steps through a 4-stage ring (128B swizzle); a
-// stage is refilled once BOTH CTAs' MMAs have read it (multicast tcgen05.commit).  tcgen05.mma
-// M=128 N=256 issued by one thread; two 256-column TMEM accumulators so the epilogue of tile i
-// overlaps the main loop of tile i+1.  Tile pairs are visited in bands of 16 pairs (32 row tiles,
-// 42 MB of x at C=5120) across all column tiles, so each band of x stays in L2 while the
-// weights stream through it once per band.
+// Kernel: persistent, clusters of two CTAs on vertically adjacent 128 x 256 output tiles.  Default
+// (OSP_PROJ_PAIR=1): a CTA pair running tcgen05.mma.cta_group::2 (M=256 across both CTAs' TMEM,
+// N=256 with each CTA holding a 128-row half of the 256 x 64 weight slice), issued by the leader
+// CTA; each CTA's TMA lands its operands in its own smem and completes on the leader's barrier;
+// 6-stage ring of 32 KB per CTA.  Alternative (OSP_PROJ_PAIR=0): two independent M=128 CTAs with
+// the weight slice TMA-multicast into both, 4 stages of 48 KB.  Either way, two 256-column TMEM
+// accumulators let the epilogue of tile i overlap the main loop of tile i+1, and tile pairs are
+// visited in bands (OSP_PROJ_BAND pairs, default 12) across all column tiles.
 #include "osp_common.cuh"
 #include "osp_internal.h"
+
+#include <cstdlib>
+#include <type_traits>
 
 namespace osp {
 namespace {
 
-constexpr int kPBM = 128, kPBN = 256, kPBK = 64, kPStages = 4, kPBand = 16;  // band in tile pairs
+constexpr int kPBM = 128, kPBN = 256, kPBK = 64, kPStages = 4;
 constexpr int kPThreads = 256;
 
 struct ProjLayout {
@@ -40,10 +42,20 @@ struct ProjLayout {
   static constexpr int kSmem = kBar + 256;
 };
 
+// CTA-pair variant: per stage each CTA holds its 128 x rows and its 128-row half of the W slice
+constexpr int kP2Stages = 6;
+struct Proj2Layout {
+  static constexpr int kA = 0;                                   // stages x 16 KB
+  static constexpr int kB = kP2Stages * kPBM * kPBK * 2;         // stages x 16 KB (W half)
+  static constexpr int kBar = kB + kP2Stages * (kPBN / 2) * kPBK * 2;
+  static constexpr int kSmem = kBar + 256;
+};
+
 struct ProjArgs {
   __nv_bfloat16* out;
   int64_t out_stride;
   int rows, chan, n_cols, n_pairs_m, n_tiles_n, k_steps;
+  int band;                 // rasterisation: tile pairs per band (all column tiles per band)
   int norm;                 // 0 none, 1 per head, 2 per token (two-phase)
   const float* gamma_q;     // (C) or null
   const float* gamma_k;
@@ -120,47 +132,58 @@ __device__ __forceinline__ void head_epilogue(float (&v)[128], const ProjArgs& a
   }
 }
 
+// kPair = false: each CTA of the cluster runs M=128 MMAs on its own tile, the W slice being
+// TMA-multicast into both.  kPair = true: the cluster is a CTA pair running cta_group::2 MMAs
+// (M=256 over both CTAs' TMEM, N=256 with each CTA holding a 128-row half of the W slice), issued
+// by the leader CTA; each CTA's TMA lands its operands in its own smem and signals the leader.
+template <bool kPair>
 __global__ void __launch_bounds__(kPThreads, 1)
     qkv_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const ProjArgs a) {
-  using Ly = ProjLayout;
+  using Ly = std::conditional_t<kPair, Proj2Layout, ProjLayout>;
+  constexpr int kStages = kPair ? kP2Stages : kPStages;
+  constexpr int kBRows = kPair ? kPBN / 2 : kPBN;   // W rows per CTA per stage
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + Ly::kBar);
-  uint64_t* bar_full = bars;                  // [stages] TMA -> MMA
-  uint64_t* bar_empty = bars + kPStages;      // [stages] MMA -> TMA
-  uint64_t* bar_acc = bars + 2 * kPStages;    // [2] MMA -> epilogue
-  uint64_t* bar_accf = bars + 2 * kPStages + 2;  // [2] epilogue -> MMA (128 arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kPStages + 4);
+  uint64_t* bar_full = bars;                  // [stages] TMA -> MMA (pair: the leader's counts)
+  uint64_t* bar_empty = bars + kStages;       // [stages] MMA -> TMA
+  uint64_t* bar_acc = bars + 2 * kStages;     // [2] MMA -> epilogue
+  uint64_t* bar_accf = bars + 2 * kStages + 2;  // [2] epilogue -> MMA (128, pair: 256 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int n_units = a.n_pairs_m * a.n_tiles_n;  // a unit = two vertically adjacent tiles
   auto tile_mn = [&](int id, int& tm, int& tn) {
-    const int band_units = kPBand * a.n_tiles_n;
+    const int band_units = a.band * a.n_tiles_n;
     const int band = id / band_units;
     const int rem = id % band_units;
-    const int pairs_in_band = min(kPBand, a.n_pairs_m - band * kPBand);
-    tm = 2 * (band * kPBand + rem % pairs_in_band) + static_cast<int>(crank);
+    const int pairs_in_band = min(a.band, a.n_pairs_m - band * a.band);
+    tm = 2 * (band * a.band + rem % pairs_in_band) + static_cast<int>(crank);
     tn = rem / pairs_in_band;
   };
 
   if ((smem_u32(sm) & 1023) != 0) __trap();
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kPStages; ++i) {
+    for (int i = 0; i < kStages; ++i) {
       mbar_init(bar_full + i, 1);
-      mbar_init(bar_empty + i, 2);  // both CTAs' MMAs read the multicast W half
+      mbar_init(bar_empty + i, kPair ? 1 : 2);  // multicast: both CTAs' MMAs read the W half
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_acc + i, 1);
-      mbar_init(bar_accf + i, 128);
+      mbar_init(bar_accf + i, kPair ? 256 : 128);
     }
     fence_barrier_init();
   }
   if (warp == 2) {
-    tmem_alloc(tmem_slot, 512);
-    tmem_relinquish();
+    if constexpr (kPair) {
+      tmem_alloc_pair(tmem_slot, 512);
+    } else {
+      tmem_alloc(tmem_slot, 512);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
   cluster_sync();
@@ -176,20 +199,29 @@ __global__ void __launch_bounds__(kPThreads, 1)
         int tm, tn;
         tile_mn(id, tm, tn);
         for (int ks = 0; ks < a.k_steps; ++ks, ++it) {
-          const int st = it % kPStages;
-          mbar_wait(bar_empty + st, ((it / kPStages) & 1) ^ 1);
-          mbar_expect_tx(bar_full + st, (kPBM + kPBN) * kPBK * 2);
-          tma_load_3d(sm + Ly::kA + st * kPBM * kPBK * 2, &tmA, bar_full + st, ks * kPBK, tm * kPBM, 0);
-          // my half of the shared W slice, delivered to both CTAs
-          tma_load_3d_multicast(sm + Ly::kB + st * kPBN * kPBK * 2 + crank * (kPBN / 2) * kPBK * 2, &tmB,
-                                bar_full + st, ks * kPBK, tn * kPBN + static_cast<int>(crank) * (kPBN / 2), 0,
-                                0x3);
+          const int st = it % kStages;
+          mbar_wait(bar_empty + st, ((it / kStages) & 1) ^ 1);
+          if constexpr (kPair) {
+            // both CTAs' A and W halves complete on the leader's full barrier
+            const uint32_t leader_full = mapa_u32(smem_u32(bar_full + st), 0);
+            if (crank == 0) mbar_expect_tx(bar_full + st, 2 * (kPBM + kBRows) * kPBK * 2);
+            tma_load_3d_pair(sm + Ly::kA + st * kPBM * kPBK * 2, &tmA, leader_full, ks * kPBK, tm * kPBM, 0);
+            tma_load_3d_pair(sm + Ly::kB + st * kBRows * kPBK * 2, &tmB, leader_full, ks * kPBK,
+                             tn * kPBN + static_cast<int>(crank) * kBRows, 0);
+          } else {
+            mbar_expect_tx(bar_full + st, (kPBM + kPBN) * kPBK * 2);
+            tma_load_3d(sm + Ly::kA + st * kPBM * kPBK * 2, &tmA, bar_full + st, ks * kPBK, tm * kPBM, 0);
+            // my half of the shared W slice, delivered to both CTAs
+            tma_load_3d_multicast(sm + Ly::kB + st * kPBN * kPBK * 2 + crank * (kPBN / 2) * kPBK * 2, &tmB,
+                                  bar_full + st, ks * kPBK, tn * kPBN + static_cast<int>(crank) * (kPBN / 2), 0,
+                                  0x3);
+          }
         }
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
-    constexpr uint32_t kId = idesc_bf16(kPBM, kPBN, 0, 0);
+  } else if (warp == 1 && (!kPair || crank == 0)) {
+    constexpr uint32_t kId = idesc_bf16(kPair ? 2 * kPBM : kPBM, kPBN, 0, 0);
     if (elect_one()) {
       int it = 0, lt = 0;
       for (int id = cluster; id < n_units; id += n_clusters, ++lt) {
@@ -198,18 +230,29 @@ __global__ void __launch_bounds__(kPThreads, 1)
         tc_fence_after();
         const uint32_t acc = tmem + buf * kPBN;
         for (int ks = 0; ks < a.k_steps; ++ks, ++it) {
-          const int st = it % kPStages;
-          mbar_wait(bar_full + st, (it / kPStages) & 1);
+          const int st = it % kStages;
+          mbar_wait(bar_full + st, (it / kStages) & 1);
           tc_fence_after();
           const uint32_t ab = smem_u32(sm + Ly::kA + st * kPBM * kPBK * 2);
-          const uint32_t bb = smem_u32(sm + Ly::kB + st * kPBN * kPBK * 2);
+          const uint32_t bb = smem_u32(sm + Ly::kB + st * kBRows * kPBK * 2);
 #pragma unroll
-          for (int kk = 0; kk < kPBK / 16; ++kk)
-            mma_ss(acc, sdesc_sw128(ab + kk * 32, 16, 1024), sdesc_sw128(bb + kk * 32, 16, 1024), kId,
-                   (ks > 0 || kk > 0) ? 1u : 0u);
-          tc_commit_multicast(bar_empty + st, 0x3);
+          for (int kk = 0; kk < kPBK / 16; ++kk) {
+            if constexpr (kPair)
+              mma_ss_pair(acc, sdesc_sw128(ab + kk * 32, 16, 1024), sdesc_sw128(bb + kk * 32, 16, 1024), kId,
+                          (ks > 0 || kk > 0) ? 1u : 0u);
+            else
+              mma_ss(acc, sdesc_sw128(ab + kk * 32, 16, 1024), sdesc_sw128(bb + kk * 32, 16, 1024), kId,
+                     (ks > 0 || kk > 0) ? 1u : 0u);
+          }
+          if constexpr (kPair)
+            tc_commit_pair(bar_empty + st, 0x3);
+          else
+            tc_commit_multicast(bar_empty + st, 0x3);
         }
-        tc_commit(bar_acc + buf);
+        if constexpr (kPair)
+          tc_commit_pair(bar_acc + buf, 0x3);
+        else
+          tc_commit(bar_acc + buf);
       }
     }
     __syncwarp();
@@ -240,7 +283,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         if (hc == kPBN / 128 - 1) {
           tc_fence_before();
-          mbar_arrive(bar_accf + buf);
+          if (kPair && crank != 0)
+            mbar_arrive_cluster(mapa_u32(smem_u32(bar_accf + buf), 0));
+          else
+            mbar_arrive(bar_accf + buf);
         }
         const int c0 = tn * kPBN + hc * 128;          // first output column of this head
         if (c0 >= a.n_cols) continue;                 // partial last column tile (3C % 256 == 128)
@@ -273,7 +319,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
   cluster_sync();  // the peer may still multicast into / arrive on this CTA until it is done
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    if constexpr (kPair)
+      tmem_dealloc_pair(tmem, 512);
+    else
+      tmem_dealloc(tmem, 512);
   }
 }
 
@@ -369,15 +418,26 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   int rc;
   CUtensorMap ma, mb;
   if ((rc = make_tmap_bf16_3d(&ma, x, chan, rows, 1, chan, kPBM)) != kOk) return rc;
-  if ((rc = make_tmap_bf16_3d(&mb, w_t, chan, n, 1, chan, kPBN / 2)) != kOk) return rc;
+  if ((rc = make_tmap_bf16_3d(&mb, w_t, chan, n, 1, chan, kPBN / 2)) != kOk) return rc;  // W half
   static bool attr_set = false;
   if (!attr_set) {
-    rc = check_cuda(cudaFuncSetAttribute(qkv_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    rc = check_cuda(cudaFuncSetAttribute(qkv_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          ProjLayout::kSmem),
                     "cudaFuncSetAttribute(qkv_gemm)");
     if (rc != kOk) return rc;
+    rc = check_cuda(cudaFuncSetAttribute(qkv_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Proj2Layout::kSmem),
+                    "cudaFuncSetAttribute(qkv_gemm pair)");
+    if (rc != kOk) return rc;
     attr_set = true;
   }
+  {
+    const char* be = getenv("OSP_PROJ_BAND");
+    a.band = be ? atoi(be) : 12;  // measured best at cfg3 (tools/bench_proj.py, OSP_PROJ_BAND)
+    if (a.band < 1) a.band = 12;
+  }
+  const char* pe = getenv("OSP_PROJ_PAIR");
+  const bool pair = pe ? atoi(pe) != 0 : true;
   if (norm == 2) {
     rc = check_cuda(cudaMemsetAsync(sumsq, 0, rows * 2 * sizeof(float), stream), "memset sumsq");
     if (rc != kOk) return rc;
@@ -389,7 +449,7 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * min(n_units, sms / 2));
   cfg.blockDim = dim3(kPThreads);
-  cfg.dynamicSmemBytes = ProjLayout::kSmem;
+  cfg.dynamicSmemBytes = pair ? Proj2Layout::kSmem : ProjLayout::kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -398,7 +458,9 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  rc = check_cuda(cudaLaunchKernelEx(&cfg, qkv_gemm_kernel, ma, mb, a), "qkv_gemm launch");
+  rc = check_cuda(pair ? cudaLaunchKernelEx(&cfg, qkv_gemm_kernel<true>, ma, mb, a)
+                       : cudaLaunchKernelEx(&cfg, qkv_gemm_kernel<false>, ma, mb, a),
+                  "qkv_gemm launch");
   if (rc != kOk || norm != 2) return rc;
   const int64_t warps = rows * 2;
   qk_norm_rope_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, stream>>>(a);
