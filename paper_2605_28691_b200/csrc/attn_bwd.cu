@@ -56,7 +56,8 @@ struct BwdArgs {
   float scale, scale_log2;
   const __nv_bfloat16* k_rows;  // K (for the TMEM copy of the key tile)
   int64_t k_row_stride;
-  int flags;  // debug experiments (OSP_BWD_FLAGS): 1 = skip dQ atomics, 2 = skip compute math
+  int flags;  // debug experiments (OSP_BWD_FLAGS): 1 = skip dQ reductions, 2 = skip compute math,
+            // 32 = per-thread vector atomics instead of the bulk reduction
 };
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -434,7 +435,12 @@ struct BwdV2Layout {
   static constexpr int kStat = kDS + 2 * 16384;       // 3 x (lse2[64], delta[64])
   static constexpr int kBar = kStat + kStages * 512;
   static constexpr int kSmem = kBar + 256;
+  // dQ^T staging for the asynchronous bulk reduction: one 64-query tile in the accumulator's
+  // (q/4, d, q%4) layout = 32 KB
+  static constexpr int kX = kSmem;
+  static constexpr int kSmemX = kX + 32768;
 };
+static_assert(BwdV2Layout::kSmemX + 1024 <= 232448, "bwd v2 smem with staging");
 
 __device__ __forceinline__ void red_add_v4_plain(float* addr, const uint32_t* v) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "r"(v[0]), "r"(v[1]),
@@ -829,6 +835,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
     const uint32_t la = static_cast<uint32_t>(wq * 32) << 16;
     const int dcol = wq * 32 + lane;
     float* acc = a.dq_acc + sh * static_cast<int64_t>(a.seq_pad) * D;
+    const bool leader = warp == 12 && lane == 0;
     for (int i = 0; i < n_q; ++i) {
       mbar_wait(bar_dq, i & 1);
       tc_fence_after();
@@ -839,14 +846,36 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       tmem_wait_ld(v1);
       tc_fence_before();
       mbar_arrive(bar_dqf);
-      if (!(a.flags & 1)) {
+      if (a.flags & 1) continue;
+      if (a.flags & 32) {  // experiment 32: per-thread vector atomics (the previous scheme)
         float* base = acc + (static_cast<int64_t>(i) * 16 * D + dcol) * 4;  // q/4 block = i*16
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) red_add_v4_plain(base + j4 * D * 4, v0 + j4 * 4);
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) red_add_v4_plain(base + (8 + j4) * D * 4, v1 + j4 * 4);
+        continue;
+      }
+      // Stage the tile in smem and hand it to one asynchronous bulk L2 reduction, so the writers
+      // never queue behind reductions: the staging buffer is reused once the previous tile's
+      // bulk reduction has read it (one tile of slack).
+      if (i >= 1) {
+        if (leader) bulk_wait_read<0>();
+        named_bar_sync(5, 128);
+      }
+      float* xs = reinterpret_cast<float*>(sm + Ly::kX) + dcol * 4;
+#pragma unroll
+      for (int j4 = 0; j4 < 8; ++j4) {
+        *reinterpret_cast<uint4*>(xs + j4 * D * 4) = make_uint4(v0[4 * j4], v0[4 * j4 + 1], v0[4 * j4 + 2], v0[4 * j4 + 3]);
+        *reinterpret_cast<uint4*>(xs + (8 + j4) * D * 4) = make_uint4(v1[4 * j4], v1[4 * j4 + 1], v1[4 * j4 + 2], v1[4 * j4 + 3]);
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(5, 128);
+      if (leader) {
+        bulk_reduce_add_f32(acc + static_cast<int64_t>(i) * 16 * D * 4, sm + Ly::kX, 32768);
+        tma_store_commit();
       }
     }
+    if (leader) tma_store_wait_all();
   }
 
   tc_fence_before();
@@ -1050,7 +1079,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
                     "cudaFuncSetAttribute(attn_bwd)");
     if (rc != kOk) return rc;
     rc = check_cuda(cudaFuncSetAttribute(attn_bwd_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         BwdV2Layout::kSmem),
+                                         BwdV2Layout::kSmemX),
                     "cudaFuncSetAttribute(attn_bwd_v2)");
     if (rc != kOk) return rc;
     attr_set = true;
@@ -1058,7 +1087,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
   dim3 grid(static_cast<unsigned>(seq_pad / 128), static_cast<unsigned>(s.heads),
             static_cast<unsigned>(s.n_seq));
   if constexpr (D == 128) {
-    attn_bwd_v2_kernel<<<grid, kBwdV2Threads, BwdV2Layout::kSmem, stream>>>(mq, mk, mv, mdo, a);
+    attn_bwd_v2_kernel<<<grid, kBwdV2Threads, BwdV2Layout::kSmemX, stream>>>(mq, mk, mv, mdo, a);
     rc = check_cuda(cudaGetLastError(), "attn_bwd_v2_kernel launch");
     if (rc != kOk) return rc;
     dq_finalize_v2_kernel<<<grid_for(s.n_seq * s.heads * seq_pad / 4 * D, 256), 256, 0, stream>>>(
