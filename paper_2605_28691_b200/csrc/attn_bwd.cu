@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 struct BwdV2Layout {
   static constexpr int kK = 0;                    // 128 keys x 128 d  (2 x 16 KB)
   static constexpr int kV = 32768;
-  static constexpr int kStages = 3;
+  static constexpr int kStages = 2;
   static constexpr int kQ = 65536;                // 3 x (64 q x 128 d = 2 x 8 KB)
   static constexpr int kDO = kQ + kStages * 16384;
   static constexpr int kDS = kDO + kStages * 16384;   // 2 x (128 keys x 64 q) bf16
@@ -437,8 +437,9 @@ struct BwdV2Layout {
   static constexpr int kSmem = kBar + 256;
   // dQ^T staging for the asynchronous bulk reduction: one 64-query tile in the accumulator's
   // (q/4, d, q%4) layout = 32 KB
+  static constexpr int kXBufs = 2;
   static constexpr int kX = kSmem;
-  static constexpr int kSmemX = kX + 32768;
+  static constexpr int kSmemX = kX + kXBufs * 32768;
 };
 static_assert(BwdV2Layout::kSmemX + 1024 <= 232448, "bwd v2 smem with staging");
 
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
   if ((smem_u32(sm) & 1023) != 0) __trap();
   if (threadIdx.x == 0) {
     mbar_init(bar_kv, 1);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < Ly::kStages; ++i) {
       mbar_init(bar_qf + i, 1);
       mbar_init(bar_qe + i, 1);
     }
@@ -552,8 +553,8 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       const CUtensorMap* mapq = lane < 16 ? &tmQ : &tmDO;
       const int base_off = lane < 16 ? Ly::kQ : Ly::kDO;
       for (int i = 0; i < n_q; ++i) {
-        const int st = i % 3;
-        mbar_wait(bar_qe + st, ((i / 3) & 1) ^ 1);
+        const int st = i % Ly::kStages;
+        mbar_wait(bar_qe + st, ((i / Ly::kStages) & 1) ^ 1);
         if (lane == 0) {
           mbar_expect_tx(bar_qf + st, 2 * 16384 + 512);
           bulk_load(sm + Ly::kStat + st * 512, lse2_g + i * 64, 256, bar_qf + st);
@@ -580,8 +581,8 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       const float* lse2_g = a.lse2 + sh * a.seq_pad;
       const float* delta_g = a.delta + sh * a.seq_pad;
       for (int i = 0; i < n_q; ++i) {
-        const int st = i % 3;
-        mbar_wait(bar_qe + st, ((i / 3) & 1) ^ 1);
+        const int st = i % Ly::kStages;
+        mbar_wait(bar_qe + st, ((i / Ly::kStages) & 1) ^ 1);
         mbar_expect_tx(bar_qf + st, 2 * 16384 + 512);
         for (int s = 0; s < 2; ++s) {
           tma_load_3d(sm + Ly::kQ + st * 16384 + s * 8192, &tmQ, bar_qf + st, head * D + s * 64,
@@ -609,7 +610,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       const uint32_t q_base0 = smem_u32(sm + Ly::kQ);
       const uint32_t do_base0 = smem_u32(sm + Ly::kDO);
       auto issue_s = [&](int i) {
-        const uint32_t qb = q_base0 + (i % 3) * 16384;
+        const uint32_t qb = q_base0 + (i % Ly::kStages) * 16384;
         {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
@@ -619,7 +620,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         }
       };
       auto issue_dp = [&](int i) {
-        const uint32_t db = do_base0 + (i % 3) * 16384;
+        const uint32_t db = do_base0 + (i % Ly::kStages) * 16384;
         {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
@@ -636,7 +637,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       issue_s(0);
       issue_dp(0);
       for (int i = 0; i < n_q; ++i) {
-        const int st = i % 3;
+        const int st = i % Ly::kStages;
         const int b = i & 1;
         const uint32_t qb = q_base0 + st * 16384;
         const uint32_t db = do_base0 + st * 16384;
@@ -651,7 +652,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         }
         // S_{i+1} (tS is free once dV_i has been issued: tcgen05 ops execute in order)
         if (i + 1 < n_q) {
-          mbar_wait(bar_qf + (i + 1) % 3, ((i + 1) / 3) & 1);
+          mbar_wait(bar_qf + (i + 1) % Ly::kStages, ((i + 1) / Ly::kStages) & 1);
           tc_fence_after();
           issue_s(i + 1);
         }
@@ -711,11 +712,11 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
     mbar_arrive(bar_kt);
     const float c = a.scale_log2;
     for (int i = 0; i < n_q; ++i) {
-      const int st = i % 3;
+      const int st = i % Ly::kStages;
       const int b = i & 1;
       const float* lse_s = reinterpret_cast<const float*>(sm + Ly::kStat + st * 512) + half * 32;
       const float* del_s = lse_s + 64;
-      mbar_wait(bar_qf + st, (i / 3) & 1);
+      mbar_wait(bar_qf + st, (i / Ly::kStages) & 1);
       // lse2 / delta of this tile's 32 query columns into registers now: shared memory is busy
       // feeding SS-mode MMAs, so these loads must not sit on the softmax critical path
       float lse_r[32], del_r[32];
@@ -858,11 +859,12 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       // Stage the tile in smem and hand it to one asynchronous bulk L2 reduction, so the writers
       // never queue behind reductions: the staging buffer is reused once the previous tile's
       // bulk reduction has read it (one tile of slack).
-      if (i >= 1) {
-        if (leader) bulk_wait_read<0>();
+      const int xb = i % Ly::kXBufs;
+      if (i >= Ly::kXBufs) {
+        if (leader) bulk_wait_read<Ly::kXBufs - 1>();
         named_bar_sync(5, 128);
       }
-      float* xs = reinterpret_cast<float*>(sm + Ly::kX) + dcol * 4;
+      float* xs = reinterpret_cast<float*>(sm + Ly::kX + xb * 32768) + dcol * 4;
 #pragma unroll
       for (int j4 = 0; j4 < 8; ++j4) {
         *reinterpret_cast<uint4*>(xs + j4 * D * 4) = make_uint4(v0[4 * j4], v0[4 * j4 + 1], v0[4 * j4 + 2], v0[4 * j4 + 3]);
@@ -871,7 +873,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       fence_proxy_async_smem();
       named_bar_sync(5, 128);
       if (leader) {
-        bulk_reduce_add_f32(acc + static_cast<int64_t>(i) * 16 * D * 4, sm + Ly::kX, 32768);
+        bulk_reduce_add_f32(acc + static_cast<int64_t>(i) * 16 * D * 4, sm + Ly::kX + xb * 32768, 32768);
         tma_store_commit();
       }
     }
