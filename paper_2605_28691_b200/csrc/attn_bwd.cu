@@ -888,30 +888,39 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
   }
 }
 
-// dq = bf16(scale * acc) from the v2 (seq*head, q/4, d, q%4) accumulator.
+// dq = bf16(scale * acc) from the v2 (seq*head, q/4, d, q%4) accumulator.  A thread takes 4
+// consecutive d of one q/4 block: one 64-byte read, four 8-byte row writes (a warp covers a whole
+// 128-d head slice, so both sides are contiguous).
 __global__ void dq_finalize_v2_kernel(const float* __restrict__ acc, __nv_bfloat16* dq, int64_t dq_stride,
                                       int64_t n_seq, int heads, int seq_len, int seq_pad, float scale,
                                       const int* __restrict__ row_index) {
   constexpr int D = 128;
   const int64_t nqb = seq_pad / 4;
-  const int64_t total = n_seq * heads * nqb * D;
+  const int64_t total = n_seq * heads * nqb * (D / 4);
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int d = static_cast<int>(i % D);
-    int64_t r = i / D;
+    const int d0 = static_cast<int>(i % (D / 4)) * 4;
+    const int64_t r = i / (D / 4);
     const int64_t qb = r % nqb;
     const int64_t sh = r / nqb;
     const int h = static_cast<int>(sh % heads);
     const int64_t s = sh / heads;
-    const float4 v = reinterpret_cast<const float4*>(acc)[i];
-    const float vv[4] = {v.x, v.y, v.z, v.w};
+    const float4* src = reinterpret_cast<const float4*>(acc) + r * D + d0;  // [d0..d0+3][q%4]
+    const float4 a0 = src[0], a1 = src[1], a2 = src[2], a3 = src[3];
+    const float col[4][4] = {{a0.x, a1.x, a2.x, a3.x}, {a0.y, a1.y, a2.y, a3.y},
+                             {a0.z, a1.z, a2.z, a3.z}, {a0.w, a1.w, a2.w, a3.w}};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t q = qb * 4 + j;
-      if (q < seq_len) {
-        const int64_t row = row_index ? row_index[s * seq_len + q] : s * seq_len + q;
-        if (row >= 0) dq[row * dq_stride + static_cast<int64_t>(h) * D + d] = __float2bfloat16(vv[j] * scale);
-      }
+      if (q >= seq_len) break;
+      const int64_t row = row_index ? row_index[s * seq_len + q] : s * seq_len + q;
+      if (row < 0) continue;
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(col[j][0] * scale, col[j][1] * scale);
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(col[j][2] * scale, col[j][3] * scale);
+      uint2 pk;
+      pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(dq + row * dq_stride + static_cast<int64_t>(h) * D + d0) = pk;
     }
   }
 }
@@ -1092,7 +1101,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     attn_bwd_v2_kernel<<<grid, kBwdV2Threads, BwdV2Layout::kSmemX, stream>>>(mq, mk, mv, mdo, a);
     rc = check_cuda(cudaGetLastError(), "attn_bwd_v2_kernel launch");
     if (rc != kOk) return rc;
-    dq_finalize_v2_kernel<<<grid_for(s.n_seq * s.heads * seq_pad / 4 * D, 256), 256, 0, stream>>>(
+    dq_finalize_v2_kernel<<<grid_for(s.n_seq * s.heads * seq_pad / 4 * (D / 4), 256), 256, 0, stream>>>(
         w.dq_acc, static_cast<__nv_bfloat16*>(dq), dqs, s.n_seq, static_cast<int>(s.heads),
         static_cast<int>(s.seq_len), static_cast<int>(seq_pad), scale, s.row_index);
     return check_cuda(cudaGetLastError(), "dq_finalize_v2 launch");
