@@ -943,10 +943,14 @@ __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t o_s
   for (int64_t wb = warp0 * R; wb < total; wb += nwarps * R) {
     const int64_t w = wb + sub;
     const bool in = w < total;
-    const int q = in ? static_cast<int>(w % seq_pad) : 0;
-    const int64_t sh = in ? w / seq_pad : 0;
-    const int h = static_cast<int>(sh % heads);
-    const int64_t s = sh / heads;
+    // 32-bit index arithmetic (64-bit division is a long software sequence); total < 2^31 is
+    // checked by the launcher
+    const uint32_t w32 = in ? static_cast<uint32_t>(w) : 0u;
+    const int q = static_cast<int>(w32 % static_cast<uint32_t>(seq_pad));
+    const uint32_t sh32 = w32 / static_cast<uint32_t>(seq_pad);
+    const int64_t sh = sh32;
+    const int h = static_cast<int>(sh32 % static_cast<uint32_t>(heads));
+    const int64_t s = sh32 / static_cast<uint32_t>(heads);
     const int len = seq_lens ? __ldg(seq_lens + s) : seq_len;
     float acc = 0.f;
     if (in && q < len) {
@@ -1026,6 +1030,10 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
   int rc = check_cuda(cudaMemsetAsync(w.dq_acc, 0, s.n_seq * seq_pad * s.heads * D * 4, stream),
                       "memset dq_acc");
   if (rc != kOk) return rc;
+  if (s.n_seq * s.heads * seq_pad >= (int64_t(1) << 31)) {
+    set_error("attention backward: n_seq * heads * padded length must stay below 2^31");
+    return kValue;
+  }
   {
     const int64_t rows = s.n_seq * s.heads * seq_pad;
     bwd_prep_kernel<D><<<grid_for(rows * 32 / (32 / (D / 8)), 256), 256, 0, stream>>>(
