@@ -132,3 +132,30 @@ def test_block_with_prologue_matches_float64_composition(P):
     want = torch.from_numpy(O.apply_table(O.map_table("gsa_to_tsa", og, 1), o2.numpy()))
     err = (y - want).abs().max().item()
     assert err < 3e-2, err
+
+
+def test_prologue_row_offset_matches_full_layout(P):
+    """An SSP shard (rows [r0, r1) of the pattern layout) gets the same q|k|v (RoPE positions
+    included) as the corresponding rows of the full-layout projection."""
+    from paper_2605_28691_b200.prologue import qkv_project
+    g = P.GridShape(2, 8, 16, 2)
+    C = 256
+    torch.manual_seed(5)
+    x = torch.randn(4, g.seq_len // 4, C, device="cuda").to(torch.bfloat16)
+    full = qkv_project(x, g, P.SparsePattern.GROUP_WISE, 1, norm="head", rope=True)
+    L = g.seq_len // 4
+    for r0, r1 in ((0, 2), (2, 4), (1, 3)):
+        part = qkv_project(x[r0:r1], g, P.SparsePattern.GROUP_WISE, 1, norm="head", rope=True,
+                           row_offset=r0 * L)
+        assert torch.equal(part, full[r0:r1])
+
+
+def test_attention_all_sequences_empty(lib):
+    from paper_2605_28691_b200 import kernels
+    q, k, v = (torch.randn(3, 256, 128, device="cuda").bfloat16() for _ in range(3))
+    sl = torch.zeros(3, dtype=torch.int32, device="cuda")
+    o, lse = kernels.attn_fwd(q, k, v, 1, 128, None, False, 0.1, seq_lens=sl)
+    assert (o == 0).all() and torch.isinf(lse).all()
+    dq, dk, dv = kernels.attn_bwd(q, k, v, o, torch.randn_like(o), lse, 1, 128, None, False, 0.1,
+                                  seq_lens=sl)
+    assert (dq == 0).all() and (dk == 0).all() and (dv == 0).all()
