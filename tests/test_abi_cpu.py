@@ -140,3 +140,20 @@ def test_ospt_and_mask_formats_byte_exact(tmp_path):
     _PG.mask = mask.cpu()
     formats.write_mask(tmp_path / "m.bin", _PG)
     assert (tmp_path / "m.bin").read_bytes() == (golden / "ref_mask_1x5x6_k2.bin").read_bytes()
+
+
+def test_integration_stub_matches_abi():
+    """The ctypes stub shown in INTEGRATION.md binds the same signatures as the package."""
+    import ctypes
+    import re
+    from pathlib import Path
+
+    from paper_2605_28691_b200 import _lib
+    text = (Path(__file__).resolve().parent.parent / "INTEGRATION.md").read_text()
+    env = {"vp": ctypes.c_void_p, "i64": ctypes.c_int64, "c_int": ctypes.c_int, "c_f": ctypes.c_float}
+    found = 0
+    for name, args in re.findall(r"_lib\.(osp_\w+)\.argtypes = \[([^\]]*)\]", text):
+        got = [eval(a.strip(), env) for a in args.split(",")]
+        assert got == _lib._SIGS[name][0], name
+        found += 1
+    assert found >= 4
