@@ -386,3 +386,22 @@ def test_block_forward_original_with_prologue(P):
     y = blk.forward_original(x)
     y.float().sum().backward()
     assert torch.isfinite(y).all() and torch.isfinite(x.grad).all()
+
+
+def test_block_head_dim_64_compaction_paths_agree(P):
+    """head_dim 64 (the v1 backward kernel) with padding compaction vs the masked block."""
+    from paper_2605_28691_b200.block import SkiparseBlock
+    g = P.GridShape(2, 10, 12, 2)
+    C, heads = 256, 4
+    a = SkiparseBlock(g, heads, C)
+    b = SkiparseBlock(g, heads, C, compact=False)
+    torch.manual_seed(6)
+    x = torch.randn(a.local_rows, a.L, C, device="cuda").to(torch.bfloat16)
+    xa, xb = x.clone().requires_grad_(True), x.clone().requires_grad_(True)
+    ya, yb = a(xa), b(xb)
+    assert (ya.float() - yb.float()).abs().max().item() < 2e-2
+    gy = torch.randn_like(ya)
+    ya.backward(gy)
+    yb.backward(gy)
+    rel = (xa.grad.float() - xb.grad.float()).abs().max().item() / xb.grad.float().abs().max().item()
+    assert rel < 2e-2, rel
