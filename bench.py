@@ -190,11 +190,50 @@ def _ncu_traffic(kernel: str):
     return (total or None), f"{Path(files[-1]).name} (one cold ncu replay, bytes per launch)"
 
 
+def _host_stage_collectives(dist) -> None:
+    import torch
+    a2a, ag, ar = dist.all_to_all_single, dist.all_gather_into_tensor, dist.all_reduce
+
+    def all_to_all_single(out, inp, group=None, **kw):
+        o = torch.empty(out.shape, dtype=out.dtype)
+        a2a(o, inp.cpu(), group=group)
+        out.copy_(o)
+
+    def all_gather_into_tensor(out, inp, group=None, **kw):
+        o = torch.empty(out.shape, dtype=out.dtype)
+        ag(o, inp.cpu(), group=group)
+        out.copy_(o)
+
+    def all_reduce(t, op=dist.ReduceOp.SUM, group=None, **kw):
+        h = t.cpu()
+        ar(h, op=op, group=group)
+        t.copy_(h)
+
+    dist.all_to_all_single, dist.all_gather_into_tensor, dist.all_reduce = (
+        all_to_all_single, all_gather_into_tensor, all_reduce)
+
+
+def _comm_summary(log, steps: int) -> dict:
+    """Measured all-to-all bytes per rank and step: the SSP switches (one per pattern switch)
+    against the Ulysses model of four all-to-alls of the same volume (ssp.py:183-226), plus the
+    Ulysses all-to-alls of an SSP x Ulysses run reported separately."""
+    steps = max(steps, 1)
+    ssp_ev = [e for e in log.events if e.label.startswith("pattern-switch")]
+    uly_ev = [e for e in log.events if e.label.startswith("ulysses")]
+    ssp_bytes = sum(e.bytes_per_rank for e in ssp_ev) // steps
+    return {"ssp_all_to_all_per_step": len(ssp_ev) // steps,
+            "ssp_bytes_per_rank_per_step": ssp_bytes,
+            "ulysses_model_bytes_per_rank_per_step": 4 * ssp_bytes,
+            "ulysses_all_to_all_per_step": len(uly_ev) // steps,
+            "ulysses_bytes_per_rank_per_step": sum(e.bytes_per_rank for e in uly_ev) // steps}
+
+
 def run_ours(args, world, rank, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2605_28691_b200 import GridShape, kernels
-    from paper_2605_28691_b200.block import SkiparseBlock, plan_parallel
+    from paper_2605_28691_b200.anyres import pad_grid
+    from paper_2605_28691_b200.block import SkiparseBlock, plan_parallel_3d
     from paper_2605_28691_b200.ssp import CommLog
 
     T, H, W, k, heads, d, desc = CONFIGS[args.config]
@@ -202,18 +241,26 @@ def run_ours(args, world, rank, local_rank):
     C = heads * d
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    group = None
-    ssp_n, dp = plan_parallel(world, k)
-    if dp > 1:
+    group = uly_group = None
+    g = GridShape(T, H, W, k)
+    pgrid = pad_grid(g).padded
+    # N <= k^2: SSP over N ranks; N > k^2: SSP (k^2) x Ulysses (N/k^2) on one latent (the paper's
+    # 8-GPU setting), or SSP x data parallel when heads / txh do not divide
+    ssp_n, uly_n, dp = plan_parallel_3d(world, k, heads, pgrid.t * pgrid.h // k2)
+    if uly_n > 1:
+        s_idx, u_idx = rank // uly_n, rank % uly_n
+        ssp_groups = [dist.new_group([s * uly_n + u for s in range(ssp_n)]) for u in range(uly_n)]
+        uly_groups = [dist.new_group([s * uly_n + u for u in range(uly_n)]) for s in range(ssp_n)]
+        group, uly_group = ssp_groups[u_idx], uly_groups[s_idx]
+    elif dp > 1:
         groups = [dist.new_group(list(range(i * ssp_n, (i + 1) * ssp_n))) for i in range(dp)]
         group = groups[rank // ssp_n]
     log = CommLog()
-    g = GridShape(T, H, W, k)
     blk = SkiparseBlock(g, heads, C, batch=1, group=group if world > 1 else None, log=log,
-                        device=dev)
+                        device=dev, ulysses_group=uly_group)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    x = torch.randn((blk.local_rows, blk.L, C), generator=gen, device=dev).to(torch.bfloat16)
-    gy = torch.randn((blk.local_rows, blk.L, C), generator=gen, device=dev).to(torch.bfloat16)
+    x = torch.randn((blk.local_rows, blk.L_local, C), generator=gen, device=dev).to(torch.bfloat16)
+    gy = torch.randn((blk.local_rows, blk.L_local, C), generator=gen, device=dev).to(torch.bfloat16)
     x.requires_grad_(True)
 
     def step(inp):
@@ -251,6 +298,7 @@ def run_ours(args, world, rank, local_rank):
     ms = e0.elapsed_time(e1)
     launches = kernels.STATS.launches
     per_kernel = kernels.STATS.elapsed_ms()
+    comm = _comm_summary(log, args.steps) if world > 1 else None   # the timed steps only
     kernels.STATS.reset(timing=False)
     t = torch.tensor([ms], device=dev)
     if world > 1:
@@ -347,7 +395,8 @@ def run_ours(args, world, rank, local_rank):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn, bf16)",
             "config": {"workload": args.config, "description": desc, "grid": [T, H, W], "k": k,
                        "heads": heads, "head_dim": d, "global_batch": dp,
-                       "parallelism": (f"ssp{ssp_n}" + (f"xdp{dp}" if dp > 1 else "")),
+                       "parallelism": (f"ssp{ssp_n}" + (f"xulysses{uly_n}" if uly_n > 1 else "")
+                                       + (f"xdp{dp}" if dp > 1 else "")),
                        "padded_grid": [blk.grid.t, blk.grid.h, blk.grid.w], "subseq_len": blk.L,
                        "l2": "inputs > 126 MB L2 (no flush needed)",
                        "block": "TSA app + switch + GSA app + switch, each app = fixed QKV "
@@ -359,10 +408,7 @@ def run_ours(args, world, rank, local_rank):
             "roofline": roof,
             "flops_per_step_per_gpu": fl,
             "kernel_ms": kern, "kernel_share_of_step": share,
-            "comm": {"all_to_all_per_step": log.count("all_to_all") // max(args.steps, 1),
-                     "bytes_per_rank_per_step": log.total_bytes() // max(args.steps, 1),
-                     "ulysses_model_bytes_per_rank_per_step":
-                         4 * log.total_bytes() // max(args.steps, 1)} if world > 1 else None,
+            "comm": comm,
             "clocks": clk.summary()}
     if world == 1 and not args.no_cpu:
         cb = cpu_oracle_rate(args.config, 1, args.cpu_sample, reps=2)
@@ -390,8 +436,17 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("OSP_BENCH_HOST_COLLECTIVES") == "1":
+            # logic check of the N-rank path on a box with fewer GPUs: all ranks share the visible
+            # GPUs and every collective is staged through the host (gloo), so no rank's kernel
+            # waits on another's.  Never used for a reported number.
+            local_rank %= torch.cuda.device_count()
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("gloo")
+            _host_stage_collectives(dist)
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, world, rank, local_rank)
     finally:

@@ -45,11 +45,28 @@ def plan_parallel(world: int, k: int) -> tuple[int, int]:
     raise ValueError(f"cannot shard k^2={k2} subsequences over {world} ranks")
 
 
+def plan_parallel_3d(world: int, k: int, heads: int, txh: int) -> tuple[int, int, int]:
+    """(SSP size, Ulysses size, data-parallel replicas).  When N > k^2 the paper's 8-GPU setting
+    composes SSP with Ulysses (SURVEY.md sec. 8e option 1): the k^2 subsequences
+    shard over k^2 SSP ranks and each subsequence's positions split over U Ulysses ranks along
+    the (t, h/k^2) "txh" axis -- the slowest index of both pattern layouts, so a position block
+    is a whole run of minimal repeatable units and the SSP switch acts on it independently.
+    Falls back to SSP x DP when heads or txh do not divide."""
+    k2 = k * k
+    if world <= k2 or world % k2:
+        s, dp = plan_parallel(world, k)
+        return s, 1, dp
+    u = world // k2
+    if heads % u == 0 and txh % u == 0:
+        return k2, u, 1
+    return k2, 1, u
+
+
 class SkiparseBlock:
     def __init__(self, g: GridShape, heads: int, chan: int, batch: int = 1, group=None,
                  log: CommLog | None = None, device=None, seeds=(PROJECTION_SEED, PROJECTION_SEED + 1),
                  transport: str = "native", qk_norm: str | None = None, rope: bool = False,
-                 eps: float = 1e-6, compact: bool = True):
+                 eps: float = 1e-6, compact: bool = True, ulysses_group=None):
         import torch.distributed as dist
         self.g = g
         self.pg: PaddedGrid = pad_grid(g)
@@ -69,6 +86,22 @@ class SkiparseBlock:
             raise ValueError(f"{n_sub * batch} subsequences do not shard over {self.world} ranks")
         self.local_rows = n_sub * batch // self.world
         self.L = self.grid.seq_len // n_sub
+        # SSP x Ulysses: this rank holds position block u of its subsequences (a txh range)
+        self.uly_group = ulysses_group
+        self.uly = dist.get_world_size(ulysses_group) if ulysses_group is not None else 1
+        self.uly_rank = dist.get_rank(ulysses_group) if ulysses_group is not None else 0
+        if self.uly > 1:
+            txh = self.grid.t * self.grid.h // n_sub
+            if qk_norm is not None or rope:
+                raise ValueError("SSP x Ulysses does not support the projection prologue")
+            if heads % self.uly or txh % self.uly:
+                raise ValueError(f"Ulysses size {self.uly} must divide heads ({heads}) and txh ({txh})")
+            self.L_local = self.L // self.uly
+            # the switch acts on one position block as on a grid of txh/U frames-rows
+            self.sub_grid = GridShape(1, txh // self.uly * n_sub, self.grid.w, g.k)
+        else:
+            self.L_local = self.L
+            self.sub_grid = self.grid
         dev = device or torch.device("cuda", torch.cuda.current_device())
         self.W1 = packed_projection(chan, COMPUTE_DTYPE, dev, seeds[0])
         self.W2 = packed_projection(chan, COMPUTE_DTYPE, dev, seeds[1])
@@ -114,16 +147,42 @@ class SkiparseBlock:
     def switch_to_gsa(self, x):
         if self.world == 1:
             return self._t2g.apply(x)
-        return ssp_switch(x, self.grid, self.group, self.log, self.transport)
+        return ssp_switch(x, self.sub_grid, self.group, self.log, self.transport)
 
     def switch_to_tsa(self, x):
         if self.world == 1:
             return self._g2t.apply(x)
-        return ssp_switch(x, self.grid, self.group, self.log, self.transport)
+        return ssp_switch(x, self.sub_grid, self.group, self.log, self.transport)
+
+    def _ulysses_in(self, qkv):
+        """(R, L/U, 3C) position block, all heads -> (R, L, 3C/U) all positions, my heads."""
+        from .stack import _UlyssesQKV
+        n = self.uly
+        h = _UlyssesQKV.apply(qkv, n, self.uly_group, self.log)            # (n*R, L/U, 3C/n)
+        R = qkv.shape[0]
+        return h.view(n, R, self.L_local, -1).transpose(0, 1).reshape(R, self.L, -1)
+
+    def _ulysses_out(self, o):
+        """(R, L, C/U) my heads -> (R, L/U, C) my position block, all heads."""
+        from .stack import _UlyssesOut
+        n = self.uly
+        R = o.shape[0]
+        rows = o.view(R, n, self.L_local, -1).transpose(0, 1).reshape(n * R, self.L_local, -1)
+        return _UlyssesOut.apply(rows, n, self.uly_group, self.log)
 
     def attend(self, x, W, bits, pattern=SparsePattern.TOKEN_WISE):
         from .compact import compact_rows, expand_rows
         plan = self.plan_tsa if pattern is SparsePattern.TOKEN_WISE else self.plan_gsa
+        if self.uly > 1:
+            # projection on my position block, Ulysses all-to-all to whole subsequences with
+            # H/U heads, compacted attention, and back
+            qkv = self._ulysses_in(torch.matmul(x, W))
+            heads = self.heads // self.uly
+            if plan is not None:
+                o = expand_rows(attention_packed(compact_rows(qkv, plan), heads, seq_lens=plan.lens), plan)
+            else:
+                o = attention_packed(qkv, heads, bits, zero_invalid_queries=bits is not None)
+            return self._ulysses_out(o)
         if self.prologue:
             from .prologue import QKVPrologue
             Wt = self.W1t if W is self.W1 else self.W2t
@@ -183,7 +242,10 @@ class SkiparseBlock:
         full = kernels.rearrange(x_orig, "orig_to_tsa", p.t, p.h, p.w, p.k, self.batch,
                                  self.g.h, self.g.w)
         r0 = self.rank * self.local_rows
-        return full[r0:r0 + self.local_rows]
+        mine = full[r0:r0 + self.local_rows]
+        if self.uly > 1:   # this rank's position block (txh range) of its subsequences
+            mine = mine[:, self.uly_rank * self.L_local:(self.uly_rank + 1) * self.L_local]
+        return mine.contiguous()
 
     def flops(self) -> dict:
         """Tensor FLOPs of one block fwd+bwd for this rank.  `attention_fwd_per_app` counts the
@@ -203,6 +265,9 @@ class SkiparseBlock:
         (f1, r1), (f2, r2) = executed(self.plan_tsa), executed(self.plan_gsa)
         proj = 2 * self.chan * 3 * self.chan  # per row: x @ [Wq|Wk|Wv]
         proj_rows = 2 * rows if self.prologue or self.plan_tsa is None else r1 + r2
+        if self.uly > 1:   # H/U heads over whole subsequences; projection on the position block
+            f1, f2 = f1 // self.uly, f2 // self.uly
+            proj_rows = 2 * self.local_rows * self.L_local
         return {
             "attention_fwd_per_app": att_fwd,
             "attention_fwd_executed": f1 + f2,           # both applications

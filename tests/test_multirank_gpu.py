@@ -144,3 +144,71 @@ def test_two_rank_hybrid_stack_matches_one_gpu(lib):
     for r in res:
         assert len(r) == 3, r
         assert r[1] < 2e-2 and r[2] < 2e-2, r
+
+
+def _sxu_worker(rank, world, port, S, U, grid, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        host_a2a = dist.all_to_all_single
+
+        def a2a(out, inp, group=None):
+            o = torch.empty(out.shape, dtype=out.dtype)
+            host_a2a(o, inp.cpu(), group=group)
+            out.copy_(o)
+
+        dist.all_to_all_single = a2a
+        from paper_2605_28691_b200 import GridShape
+        from paper_2605_28691_b200.block import SkiparseBlock
+        from paper_2605_28691_b200.ssp import CommLog
+        s_idx, u_idx = rank // U, rank % U
+        ssp_groups = [dist.new_group([s * U + u for s in range(S)]) for u in range(U)]
+        uly_groups = [dist.new_group([s * U + u for u in range(U)]) for s in range(S)]
+        solo_group = dist.new_group([rank])
+        g = GridShape(*grid)
+        C, heads = 256, 2
+        log = CommLog()
+        blk = SkiparseBlock(g, heads, C, group=ssp_groups[u_idx], ulysses_group=uly_groups[s_idx], log=log)
+        solo = SkiparseBlock(g, heads, C, group=solo_group)
+        assert blk.world == S and blk.uly == U
+        torch.manual_seed(0)
+        x_full = torch.randn(solo.local_rows, solo.L, C, device="cuda").to(torch.bfloat16)
+        gy_full = torch.randn_like(x_full)
+        r0, r1 = s_idx * blk.local_rows, (s_idx + 1) * blk.local_rows
+        p0, p1 = u_idx * blk.L_local, (u_idx + 1) * blk.L_local
+        xs = x_full.clone().requires_grad_(True)
+        ys = solo(xs)
+        ys.backward(gy_full)
+        xl = x_full[r0:r1, p0:p1].clone().requires_grad_(True)
+        yl = blk(xl)
+        yl.backward(gy_full[r0:r1, p0:p1].contiguous())
+        e_f = (yl.float() - ys[r0:r1, p0:p1].float()).abs().max().item() / ys.float().abs().max().item()
+        e_b = ((xl.grad.float() - xs.grad[r0:r1, p0:p1].float()).abs().max().item()
+               / xs.grad.float().abs().max().item())
+        kinds = sorted({e.label for e in log.events})
+        q.put((rank, e_f, e_b, kinds))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("S,U,grid", [(2, 2, (2, 8, 16, 2)), (4, 2, (2, 10, 12, 2))])
+def test_ssp_x_ulysses_block_matches_one_gpu(lib, S, U, grid):
+    """SSP x Ulysses (the paper's 8-GPU composition) as S*U ranks sharing the GPU: each rank's
+    position block of its subsequences equals the one-GPU block, fwd and input gradient."""
+    world = S * U
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sxu_worker, args=(r, world, port, S, U, grid, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert len(r) == 4, r
+        assert r[1] < 2e-2 and r[2] < 2e-2, r
+        assert "pattern-switch" in r[3] and "ulysses-qkv" in r[3], r

@@ -165,3 +165,24 @@ def test_ulysses_all_to_all_over_gloo(world):
         p.join(timeout=60)
     for r in res:
         assert len(r) == 5 and all(r[1:]), r
+
+
+def test_switch_on_position_blocks_equals_restriction_of_full_switch():
+    """SSP x Ulysses premise: a contiguous block of the txh = t*H/k^2 + h/k^2 axis is a run of
+    whole rows in both pattern layouts, and the SSP switch of that block on the sub-grid
+    (1, txh_block*k^2, W, k) equals the full-grid switch restricted to the block."""
+    for grid, n, U in [((2, 8, 16, 2), 2, 2), ((3, 8, 8, 2), 4, 2), ((1, 16, 16, 2), 2, 4),
+                       ((2, 16, 32, 4), 4, 2)]:
+        g = O.Grid(*grid)
+        k2 = g.k * g.k
+        txh = g.t * g.h // k2
+        L = g.seq_len // k2
+        Lu = L // U
+        rng = np.random.default_rng(sum(grid))
+        x = rng.standard_normal((k2, L, 3))
+        full = O.ssp_switch(O.shard(x, n), g)
+        sub = O.Grid(1, txh // U * k2, g.w, g.k)
+        for u in range(U):
+            blk = O.ssp_switch(O.shard(np.ascontiguousarray(x[:, u * Lu:(u + 1) * Lu]), n), sub)
+            for r in range(n):
+                assert np.array_equal(blk[r], full[r][:, u * Lu:(u + 1) * Lu]), (grid, n, U, u, r)
