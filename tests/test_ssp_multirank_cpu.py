@@ -95,6 +95,13 @@ def test_plan_parallel():
     assert plan_parallel(8, 4) == (8, 1)   # k=4: 16 subsequences over 8 ranks
     with pytest.raises(ValueError):
         plan_parallel(3, 2)
+    from paper_2605_28691_b200.block import plan_parallel_3d
+    assert plan_parallel_3d(1, 2, 40, 252) == (1, 1, 1)
+    assert plan_parallel_3d(4, 2, 40, 252) == (4, 1, 1)
+    assert plan_parallel_3d(8, 2, 40, 252) == (4, 2, 1)     # SSP4 x Ulysses2 (paper setting)
+    assert plan_parallel_3d(8, 2, 40, 251) == (4, 1, 2)     # txh odd: SSP4 x DP2
+    assert plan_parallel_3d(8, 2, 3, 252) == (4, 1, 2)      # heads not divisible
+    assert plan_parallel_3d(8, 4, 40, 63) == (8, 1, 1)      # k=4: plain SSP8
 
 
 def test_check_switch_guards():
