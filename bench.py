@@ -221,9 +221,11 @@ def _comm_summary(log, steps: int) -> dict:
     ssp_ev = [e for e in log.events if e.label.startswith("pattern-switch")]
     uly_ev = [e for e in log.events if e.label.startswith("ulysses")]
     ssp_bytes = sum(e.bytes_per_rank for e in ssp_ev) // steps
+    shard_bytes = 2 * sum(e.payload_per_rank for e in ssp_ev) // steps   # bf16 shard per switch
     return {"ssp_all_to_all_per_step": len(ssp_ev) // steps,
+            # native: the whole send buffer; hif8: its 8-bit codes; p2p: real rows pulled from peers
             "ssp_bytes_per_rank_per_step": ssp_bytes,
-            "ulysses_model_bytes_per_rank_per_step": 4 * ssp_bytes,
+            "ulysses_model_bytes_per_rank_per_step": 4 * shard_bytes,
             "ulysses_all_to_all_per_step": len(uly_ev) // steps,
             "ulysses_bytes_per_rank_per_step": sum(e.bytes_per_rank for e in uly_ev) // steps}
 
@@ -256,8 +258,13 @@ def run_ours(args, world, rank, local_rank):
         groups = [dist.new_group(list(range(i * ssp_n, (i + 1) * ssp_n))) for i in range(dp)]
         group = groups[rank // ssp_n]
     log = CommLog()
+    # the SSP switch: one pull over NVLink peer memory (K7) when SSP alone shards the latent;
+    # NCCL all-to-all around the Ulysses groups
+    transport = args.transport
+    if transport == "auto":
+        transport = "p2p" if world > 1 and uly_n == 1 else "native"
     blk = SkiparseBlock(g, heads, C, batch=1, group=group if world > 1 else None, log=log,
-                        device=dev, ulysses_group=uly_group)
+                        device=dev, ulysses_group=uly_group, transport=transport)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     x = torch.randn((blk.local_rows, blk.L_local, C), generator=gen, device=dev).to(torch.bfloat16)
     gy = torch.randn((blk.local_rows, blk.L_local, C), generator=gen, device=dev).to(torch.bfloat16)
@@ -299,6 +306,8 @@ def run_ours(args, world, rank, local_rank):
     launches = kernels.STATS.launches
     per_kernel = kernels.STATS.elapsed_ms()
     comm = _comm_summary(log, args.steps) if world > 1 else None   # the timed steps only
+    if comm is not None:
+        comm["ssp_transport"] = transport
     kernels.STATS.reset(timing=False)
     t = torch.tensor([ms], device=dev)
     if world > 1:
@@ -426,6 +435,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=2048)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--transport", default="auto", choices=["auto", "native", "hif8", "p2p"],
+                    help="SSP switch transport for N > 1 (auto: p2p pull unless Ulysses is on)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -444,6 +455,7 @@ def main():
             torch.cuda.set_device(local_rank)
             dist.init_process_group("gloo")
             _host_stage_collectives(dist)
+            os.environ["OSP_PEER_HOST_SYNC"] = "1"
         else:
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))

@@ -217,6 +217,28 @@ int osp_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, int
                     int64_t w, int64_t k, int pattern, int64_t batch, int64_t row_offset,
                     void* stream);
 
+/*
+ * K7: the SSP pattern switch as one pull over peer memory (replaces pack -> all_to_all -> unpack,
+ * ssp.py:156-178, for the block's switches).
+ *   osp_peer_alloc / osp_peer_free: a zeroed cudaMalloc buffer that can be exported over CUDA IPC.
+ *   osp_peer_export: its 64-byte cudaIpcMemHandle; osp_peer_import opens a peer's handle
+ *                    (lazy peer access), osp_peer_close releases it.
+ *   osp_peer_barrier: flag_blocks = host array of n device pointers, rank j's uint32[n] flag
+ *                    block; publishes `epoch` to slot `rank` of every block and waits until every
+ *                    slot of this rank's block reached it (epochs increase by one per barrier).
+ *   osp_peer_gather: dst[i] = row (table[i] % stride_rows) of srcs[table[i] / stride_rows]
+ *                    (srcs = host array of n_src device pointers, local or peer-mapped);
+ *                    table[i] < 0 gives a zero row.  table is a device int64 array of n_rows.
+ */
+int osp_peer_alloc(int64_t bytes, void** ptr);
+int osp_peer_free(void* ptr);
+int osp_peer_export(void* ptr, uint8_t* handle64);
+int osp_peer_import(const uint8_t* handle64, void** ptr);
+int osp_peer_close(void* ptr);
+int osp_peer_barrier(const void* const* flag_blocks, int rank, int n, uint32_t epoch, void* stream);
+int osp_peer_gather(const void* const* srcs, int n_src, int64_t stride_rows, const int64_t* table,
+                    int64_t n_rows, void* dst, int64_t row_bytes, void* stream);
+
 /* Self-test of the tcgen05 instruction forms (S = A B^T, O = bf16(S) V for one 128-row tile). */
 int osp_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,
                   int64_t head_dim, void* stream);

@@ -54,6 +54,13 @@ _SIGS = {
     "osp_hif8_scale": ([c_vp, c_i64, ctypes.c_double, ctypes.c_double, c_vp, c_vp], c_int),
     "osp_hif8_encode": ([c_vp, c_int, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp], c_int),
     "osp_hif8_decode": ([c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_int, c_vp], c_int),
+    "osp_peer_alloc": ([c_i64, c_vp], c_int),
+    "osp_peer_free": ([c_vp], c_int),
+    "osp_peer_export": ([c_vp, c_vp], c_int),
+    "osp_peer_import": ([c_vp, c_vp], c_int),
+    "osp_peer_close": ([c_vp], c_int),
+    "osp_peer_barrier": ([c_vp, c_int, c_int, ctypes.c_uint32, c_vp], c_int),
+    "osp_peer_gather": ([c_vp, c_int, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp], c_int),
     "osp_debug_mma": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp], c_int),
 }
 

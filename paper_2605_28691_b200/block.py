@@ -143,6 +143,35 @@ class SkiparseBlock:
             self._fused = (row_move(a, pt.n_seq * pt.cap, pgs.cap, pt.cap),
                            row_move(b, pgs.n_seq * pgs.cap, pt.L, pgs.cap))
 
+        # N GPUs, transport "p2p": each switch is one pull over peer memory (K7, peer.py) whose
+        # table folds expand -> switch -> compact; every rank builds every rank's plans
+        self._peer = None
+        if transport == "p2p":
+            if self.world == 1:
+                pass
+            elif self.uly > 1 or not compact:
+                raise ValueError("the p2p switch needs compaction and no Ulysses group")
+            else:
+                from .compact import compact_plan
+                from .peer import block_switch_moves, shared_arena
+                rng = [(j * self.local_rows, (j + 1) * self.local_rows) for j in range(self.world)]
+                if self.pg.trivial:   # no pad tokens: identity plans (every row real)
+                    full = compact_plan(torch.ones(self.local_rows, self.L, dtype=torch.bool, device=dev))
+                    pts = pgs = [full] * self.world
+                    self.plan_tsa = self.plan_gsa = full
+                else:
+                    pts = [self.pg.compact_plan(SparsePattern.TOKEN_WISE, batch, r) for r in rng]
+                    pgs = [self.pg.compact_plan(SparsePattern.GROUP_WISE, batch, r) for r in rng]
+                A, B = block_switch_moves(self.world, self.rank, self.local_rows, self.L,
+                                          self._t2g.src.reshape(-1).to(dev),
+                                          self._g2t.src.reshape(-1).to(dev), pts, pgs,
+                                          padded_gsa=self.prologue)
+                self._peer = (A, B)
+                row_bytes = chan * torch.finfo(COMPUTE_DTYPE).bits // 8
+                slot_rows = max(max(p.n_seq * p.cap for p in pts), max(p.n_seq * p.cap for p in pgs),
+                                self.local_rows * self.L)
+                self.arena = shared_arena(self.group, slot_rows * row_bytes)
+
     # ------------------------------------------------------------------ pieces
     def switch_to_gsa(self, x):
         if self.world == 1:
@@ -170,7 +199,10 @@ class SkiparseBlock:
         rows = o.view(R, n, self.L_local, -1).transpose(0, 1).reshape(n * R, self.L_local, -1)
         return _UlyssesOut.apply(rows, n, self.uly_group, self.log)
 
-    def attend(self, x, W, bits, pattern=SparsePattern.TOKEN_WISE):
+    def attend(self, x, W, bits, pattern=SparsePattern.TOKEN_WISE, compact_in=False, expand=True):
+        """One attention application on this rank's shard.  compact_in: x already holds the
+        compacted rows; expand=False: return the compacted output (the peer switch moves
+        compact rows directly)."""
         from .compact import compact_rows, expand_rows
         plan = self.plan_tsa if pattern is SparsePattern.TOKEN_WISE else self.plan_gsa
         if self.uly > 1:
@@ -193,11 +225,12 @@ class SkiparseBlock:
             if plan is not None:
                 qkv = compact_rows(qkv, plan)
         elif plan is not None:
-            qkv = torch.matmul(compact_rows(x, plan), W)
+            qkv = torch.matmul(x if compact_in else compact_rows(x, plan), W)
         else:
             qkv = torch.matmul(x, W)
         if plan is not None:
-            return expand_rows(attention_packed(qkv, self.heads, seq_lens=plan.lens), plan)
+            o = attention_packed(qkv, self.heads, seq_lens=plan.lens)
+            return expand_rows(o, plan) if expand else o
         return attention_packed(qkv, self.heads, bits, zero_invalid_queries=bits is not None)
 
     def forward_original(self, x: torch.Tensor) -> torch.Tensor:
@@ -225,10 +258,21 @@ class SkiparseBlock:
         o2 = attention_packed(torch.matmul(x2, self.W2), self.heads, seq_lens=pgs.lens)
         return apply_move(o2, self._fused[1])
 
+    def _call_peer(self, x_tsa):
+        from .peer import peer_switch
+        A, B = self._peer
+        o1 = self.attend(x_tsa, self.W1, self.bits_tsa, expand=False)
+        x2 = peer_switch(o1, A, self.arena, self.log)
+        o2 = self.attend(x2, self.W2, self.bits_gsa, SparsePattern.GROUP_WISE,
+                         compact_in=not self.prologue, expand=False)
+        return peer_switch(o2, B, self.arena, self.log)
+
     def __call__(self, x_tsa: torch.Tensor) -> torch.Tensor:
         """x_tsa: this rank's (G*B, L, C) bf16 shard in the token-wise layout."""
         if self._fused is not None:
             return self._call_fused(x_tsa)
+        if self._peer is not None:
+            return self._call_peer(x_tsa)
         o1 = self.attend(x_tsa, self.W1, self.bits_tsa)
         x2 = self.switch_to_gsa(o1)
         o2 = self.attend(x2, self.W2, self.bits_gsa, SparsePattern.GROUP_WISE)

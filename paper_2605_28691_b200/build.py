@@ -11,7 +11,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = Path(os.environ["OSP_LIB_OUT"]) if os.environ.get("OSP_LIB_OUT") else PKG / "libosp_skiparse.so"
-SOURCES = ["abi.cu", "rearrange.cu", "attn_fwd.cu", "attn_bwd.cu", "hif8.cu", "proj.cu", "debug_mma.cu"]
+SOURCES = ["abi.cu", "rearrange.cu", "attn_fwd.cu", "attn_bwd.cu", "hif8.cu", "proj.cu", "peer.cu", "debug_mma.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

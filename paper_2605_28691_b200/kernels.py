@@ -109,6 +109,38 @@ def gather_rows(x: torch.Tensor, index: torch.Tensor, n_out_rows: int) -> torch.
     return out
 
 
+def _ptr_array(ptrs) -> "ctypes.Array":
+    import ctypes
+    return (ctypes.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+
+
+def peer_gather(src_ptrs, stride_rows: int, table: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """K7: out row i = row (table[i] % stride) of source buffer src_ptrs[table[i] // stride]
+    (device addresses, local or peer-mapped); table[i] < 0 -> zero row."""
+    L = _lib.lib()
+    _cuda(out, "out")
+    if not out.is_contiguous():
+        raise ShapeError("peer_gather output must be contiguous")
+    table = table.to(device=out.device, dtype=torch.int64).contiguous()
+    n_rows = table.numel()
+    row_bytes = out.numel() // max(n_rows, 1) * out.element_size() if n_rows else 0
+    if n_rows and out.numel() % n_rows:
+        raise ShapeError("output does not split into table rows")
+    arr = _ptr_array(src_ptrs)
+    _lib.check(STATS.run('peer_gather', 1, lambda: L.osp_peer_gather(
+        arr, len(src_ptrs), stride_rows, table.data_ptr(), n_rows, out.data_ptr(), row_bytes,
+        _lib.stream_ptr(out.device))))
+    return out
+
+
+def peer_barrier(flag_ptrs, rank: int, epoch: int, device=None) -> None:
+    """K7: device-side flag barrier over the peers' flag blocks (see include/osp_skiparse.h)."""
+    L = _lib.lib()
+    arr = _ptr_array(flag_ptrs)
+    _lib.check(STATS.run('peer_barrier', 1, lambda: L.osp_peer_barrier(
+        arr, rank, len(flag_ptrs), epoch & 0xFFFFFFFF, _lib.stream_ptr(device))))
+
+
 def invert_index(index: torch.Tensor) -> torch.Tensor:
     L = _lib.lib()
     _cuda(index, "index")
