@@ -29,7 +29,8 @@ import torch
 
 from . import _lib, kernels
 
-__all__ = ["PeerArena", "PeerMove", "peer_move", "shared_arena", "peer_switch", "block_switch_moves"]
+__all__ = ["PeerArena", "PeerMove", "peer_move", "shared_arena", "peer_switch", "block_switch_moves",
+           "padded_switch_moves"]
 
 
 class _Mem:
@@ -200,6 +201,17 @@ def block_switch_moves(world: int, rank: int, local_rows: int, L: int, t2g: torc
     b_dst = [enc_g[g2t[r * LR + torch.arange(LR, device=dev, dtype=torch.int64)]] for r in range(world)]
     B = peer_move(b_dst, rows_g, rank, L, plans_gsa[rank].cap)
     return A, B
+
+
+def padded_switch_moves(world: int, rank: int, local_rows: int, L: int, t2g: torch.Tensor,
+                        g2t: torch.Tensor) -> tuple[PeerMove, PeerMove]:
+    """Plain switches between padded layouts (HybridStack): (TSA -> GSA, GSA -> TSA)."""
+    from .compact import compact_plan
+    full = compact_plan(torch.ones(local_rows, L, dtype=torch.bool, device=t2g.device))
+    plans = [full] * world
+    to_gsa, to_tsa = block_switch_moves(world, rank, local_rows, L, t2g, g2t, plans, plans,
+                                        padded_gsa=True)
+    return to_gsa, to_tsa
 
 
 class _PeerSwitch(torch.autograd.Function):

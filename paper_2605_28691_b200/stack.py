@@ -112,7 +112,7 @@ class HybridStack:
 
     def __init__(self, g: GridShape, heads: int, chan: int, schedule=None, num_layers: int = 6,
                  n_full: int = 2, batch: int = 1, group=None, log: CommLog | None = None,
-                 device=None, seed: int = PROJECTION_SEED):
+                 device=None, seed: int = PROJECTION_SEED, transport: str = "native"):
         import torch.distributed as dist
         self.schedule = list(schedule) if schedule is not None else build_layer_schedule(num_layers, n_full)
         self.g, self.pg = g, pad_grid(g)
@@ -148,12 +148,29 @@ class HybridStack:
                            for pat, fb in self.full_bits.items()}
         self._t2g = IndexMap._pattern("tsa_to_gsa", self.grid, batch)
         self._g2t = IndexMap._pattern("gsa_to_tsa", self.grid, batch)
+        # transport "p2p": each switch is one pull over peer memory (K7, peer.py)
+        self.transport = transport
+        self._peer = None
+        if transport == "p2p" and self.world > 1:
+            from .peer import padded_switch_moves, shared_arena
+            self._peer = padded_switch_moves(self.world, self.rank, self.local_rows, self.L,
+                                             self._t2g.src.reshape(-1).to(dev),
+                                             self._g2t.src.reshape(-1).to(dev))
+            row_bytes = chan * torch.finfo(COMPUTE_DTYPE).bits // 8
+            self.arena = shared_arena(group, self.local_rows * self.L * row_bytes)
+        elif transport not in ("native", "hif8", "p2p"):
+            raise ValueError(f"unknown transport {transport!r}")
 
     # ------------------------------------------------------------------ pieces
     def _switch(self, x, to: SparsePattern):
         if self.world == 1:
             return (self._t2g if to is SparsePattern.GROUP_WISE else self._g2t).apply(x)
-        return ssp_switch(x, self.grid, self.group, self.log)
+        if self._peer is not None:
+            from .peer import peer_switch
+            return peer_switch(x, self._peer[0 if to is SparsePattern.GROUP_WISE else 1], self.arena,
+                               self.log)
+        return ssp_switch(x, self.grid, self.group, self.log,
+                          "hif8" if self.transport == "hif8" else "native")
 
     def _skiparse(self, x, W, pat):
         from .compact import compact_rows, expand_rows

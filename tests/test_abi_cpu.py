@@ -150,7 +150,8 @@ def test_integration_stub_matches_abi():
 
     from paper_2605_28691_b200 import _lib
     text = (Path(__file__).resolve().parent.parent / "INTEGRATION.md").read_text()
-    env = {"vp": ctypes.c_void_p, "i64": ctypes.c_int64, "c_int": ctypes.c_int, "c_f": ctypes.c_float}
+    env = {"vp": ctypes.c_void_p, "i64": ctypes.c_int64, "c_int": ctypes.c_int, "c_f": ctypes.c_float,
+           "ctypes": ctypes}
     found = 0
     for name, args in re.findall(r"_lib\.(osp_\w+)\.argtypes = \[([^\]]*)\]", text):
         got = [eval(a.strip(), env) for a in args.split(",")]

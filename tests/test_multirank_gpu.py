@@ -102,9 +102,10 @@ def test_two_rank_block_matches_one_gpu_block(lib, grid, transport):
         assert n_a2a == 4   # 2 switches forward + 2 backward, one all-to-all (or pull) each
 
 
-def _stack_worker(rank, world, port, q):
+def _stack_worker(rank, world, port, q, transport="native"):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        os.environ["OSP_PEER_HOST_SYNC"] = "1"
         torch.cuda.set_device(0)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         host_a2a = dist.all_to_all_single
@@ -119,7 +120,7 @@ def _stack_worker(rank, world, port, q):
         from paper_2605_28691_b200.stack import HybridStack
         g = GridShape(2, 10, 12, 2)
         C, heads = 256, 2
-        st = HybridStack(g, heads, C, num_layers=4, n_full=2)     # FULL, TSA, GSA, FULL
+        st = HybridStack(g, heads, C, num_layers=4, n_full=2, transport=transport)  # FULL, TSA, GSA, FULL
         solo = HybridStack(g, heads, C, num_layers=4, n_full=2, group=dist.new_group([rank]))
         torch.manual_seed(1)
         x_full = torch.randn(solo.local_rows, solo.L, C, device="cuda").to(torch.bfloat16)
@@ -141,12 +142,13 @@ def _stack_worker(rank, world, port, q):
         q.put((rank, traceback.format_exc()))
 
 
-def test_two_rank_hybrid_stack_matches_one_gpu(lib):
+@pytest.mark.parametrize("transport", ["native", "p2p"])
+def test_two_rank_hybrid_stack_matches_one_gpu(lib, transport):
     """FULL blocks with Ulysses head parallelism + SSP-switched TSA/GSA blocks on 2 ranks."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_stack_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_stack_worker, args=(r, 2, port, q, transport)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(2)]
