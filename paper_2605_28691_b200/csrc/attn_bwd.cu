@@ -417,7 +417,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // Main kernel for head_dim 128.  One CTA per (128-key tile, head, subsequence) streams 64-query
 // tiles.  Shared-memory operand bandwidth (128 B/clk/SM for tcgen05 SS mode, measured with
 // tools/mma_rate.cu) is the binding resource, so operands that can live in TMEM do:
-//   TMEM: [0,64) K (A operand of S^T, copied once), [64,128) S^T then P^T,
+//   TMEM: [0,64) K (A operand of S^T, copied once), [64,128) S^T then P^T (query half h
+//         packed at [64 + 32h, 80 + 32h)),
 //         [128,192) dP^T then dS^T, [192,256) dQ^T, [256,384) dV, [384,512) dK.
 //   S^T = K Q^T (TS), dP^T = V dO^T (SS), dV += P^T dO (TS), dK += dS^T Q (TS),
 //   dQ^T_i = K^T dS_i^T (SS, dS^T also staged in smem as the B operand).
@@ -647,8 +648,8 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_ts(mDV, mS + kk * 8, sdesc_sw128(db + kk * 2048, 8192, 1024), kIdKV,
-                   (i > 0 || kk > 0) ? 1u : 0u);
+            mma_ts(mDV, mS + (kk >> 1) * 32 + (kk & 1) * 8, sdesc_sw128(db + kk * 2048, 8192, 1024),
+                   kIdKV, (i > 0 || kk > 0) ? 1u : 0u);
         }
         // S_{i+1} (tS is free once dV_i has been issued: tcgen05 ops execute in order)
         if (i + 1 < n_q) {
@@ -761,7 +762,10 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(p[2 * j], p[2 * j + 1]);
-        tmem_st16(tS + la + half * 16, pk);
+        // P^T of query half h goes to columns [32h, 32h + 16): inside the S^T columns this
+        // warpgroup itself read, never over the other warpgroup's, which may still be loading
+        // them (placing half 1 at [16, 32) raced with half 0's S^T load)
+        tmem_st16(tS + la + half * 32, pk);
       }
       tmem_wait_st();
       tc_fence_before();
