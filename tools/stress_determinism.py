@@ -39,3 +39,43 @@ for r in range(a.reps):
         bad += 1
         print(f"rep {r}: o/lse/dk/dv identical {same[0]} {same[1]} {same[3]} {same[4]}, dq rel dev {dq_err:.2e}")
 print(f"{a.reps} reps, {bad} deviating")
+
+# K6 projection (CTA-pair GEMM + norm/RoPE epilogue) and the gather-mode attention
+from paper_2605_28691_b200 import GridShape, SparsePattern, pad_grid
+from paper_2605_28691_b200.compact import gather_plan
+from paper_2605_28691_b200.prologue import qkv_project
+
+g = GridShape(21, 30, 52, 2)
+pg = pad_grid(g)
+x = torch.randn(pg.padded.seq_len, C, device="cuda").bfloat16()
+bad = 0
+refp = None
+for r in range(a.reps // 2):
+    outs = [qkv_project(x, pg.padded, SparsePattern.TOKEN_WISE, 1, norm, rope=True)
+            for norm in (None, "head", "channel")]
+    if refp is None:
+        refp = outs
+        continue
+    for name, u, w in zip(("plain", "head", "channel"), outs, refp):
+        if not torch.equal(u, w):
+            dev = ((u.float() - w.float()).abs() / (w.float().abs() + 1e-3)).max().item()
+            print(f"K6 {name}: rep {r} deviates, max rel {dev:.2e}")
+            bad += name != "channel" or dev > 2 ** -6   # channel: fp32 sum-of-squares order
+print(f"K6: {a.reps // 2} reps, {bad} deviating")
+plan = gather_plan(g, SparsePattern.GROUP_WISE, 1, pg, "original")
+xs = torch.randn(plan.n_rows, 3 * C, device="cuda").bfloat16()
+qg, kg, vg = xs[:, :C], xs[:, C:2 * C], xs[:, 2 * C:]
+dog = torch.randn(plan.n_rows, C, device="cuda").bfloat16()
+bad = 0
+refg = None
+for r in range(a.reps // 2):
+    o, lse = kernels.attn_fwd_gather(qg, kg, vg, H, d, plan.row_index, plan.lens, sc)
+    dq, dk, dv = kernels.attn_bwd_gather(qg, kg, vg, o, dog, lse, H, d, plan.row_index, plan.lens, sc)
+    cur = (o.clone(), dk.clone(), dv.clone(), dq.float())
+    if refg is None:
+        refg = cur
+        continue
+    if not (torch.equal(cur[0], refg[0]) and torch.equal(cur[1], refg[1]) and torch.equal(cur[2], refg[2])
+            and torch.allclose(cur[3], refg[3], rtol=2 ** -6, atol=1e-6)):
+        bad += 1
+print(f"gather mode: {a.reps // 2} reps, {bad} deviating")
