@@ -184,7 +184,7 @@ def _ncu_traffic(kernel: str):
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     total = 0.0
     for line in Path(files[-1]).read_text().splitlines():
-        m = re.match(r"dram__bytes_(read|write)\.sum = ([0-9.]+) (\w+)", line)
+        m = re.match(r"dram__bytes_(read|write)\.sum = ([0-9.]+) (\w+)", line.strip())
         if m:
             total += float(m.group(2)) * units.get(m.group(3), 1)
     return (total or None), f"{Path(files[-1]).name} (one cold ncu replay, bytes per launch)"
@@ -347,7 +347,8 @@ def run_ours(args, world, rank, local_rank):
         stream.wait_event(ready[b])
         xin = bufs[b].detach().requires_grad_(True)
         y = blk(xin)
-        loss = (y.float() * gy.float()).sum()
+        # the step's scalar loss <y, gy> as one GEMV pass (fp32 accumulate), read back below
+        loss = torch.mm(y.detach().reshape(1, -1), gy.reshape(-1, 1)).float()
         y.backward(gy)
         consumed[b].record(stream)
         host_loss[i:i + 1].copy_(loss.detach().view(1), non_blocking=True)
