@@ -57,7 +57,7 @@ struct BwdArgs {
   const __nv_bfloat16* k_rows;  // K (for the TMEM copy of the key tile)
   int64_t k_row_stride;
   int flags;  // debug experiments (OSP_BWD_FLAGS): 1 = skip dQ reductions, 2 = skip compute math,
-            // 32 = per-thread vector atomics instead of the bulk reduction
+            // 32 = per-thread vector atomics instead of the bulk reduction, 64 = no Q/dO reloads
 };
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -584,6 +584,10 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       for (int i = 0; i < n_q; ++i) {
         const int st = i % Ly::kStages;
         mbar_wait(bar_qe + st, ((i / Ly::kStages) & 1) ^ 1);
+        if ((a.flags & 64) && i >= 2) {  // experiment 64: no Q/dO reloads (stale tiles, timing only)
+          mbar_arrive(bar_qf + st);
+          continue;
+        }
         mbar_expect_tx(bar_qf + st, 2 * 16384 + 512);
         for (int s = 0; s < 2; ++s) {
           tma_load_3d(sm + Ly::kQ + st * 16384 + s * 8192, &tmQ, bar_qf + st, head * D + s * 64,

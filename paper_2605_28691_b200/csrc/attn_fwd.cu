@@ -55,7 +55,7 @@ struct FwdArgs {
   float scale_log2;
   int zero_invalid_q;
   int flags;  // debug experiments (OSP_FWD_FLAGS): 1 = no exp, 2 = softmax skeleton only,
-             // 4 = no exp-phase ping-pong
+             // 4 = no exp-phase ping-pong, 8 = no K/V reloads
 };
 
 __device__ __forceinline__ bool bit_at(const uint32_t* bits, int words, int i) {
@@ -174,6 +174,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
         const uint32_t ph = (j >> 1) & 1;
+        if ((a.flags & 8) && j >= 2) {  // experiment 8: no K/V reloads (stale tiles, timing only)
+          mbar_wait(bar_ke + st, ph ^ 1);
+          mbar_arrive(bar_kf + st);
+          mbar_wait(bar_ve + st, ph ^ 1);
+          mbar_arrive(bar_vf + st);
+          continue;
+        }
         mbar_wait(bar_ke + st, ph ^ 1);
         mbar_expect_tx(bar_kf + st, Ly::kTile);
 #pragma unroll
