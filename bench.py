@@ -262,7 +262,11 @@ def run_ours(args, world, rank, local_rank):
     # NCCL all-to-all around the Ulysses groups
     transport = args.transport
     if transport == "auto":
-        transport = "p2p" if world > 1 and uly_n == 1 else "native"
+        # p2p needs every rank's GPU to map every peer's memory (one NVLink / NVSwitch domain)
+        peers_ok = world > 1 and all(
+            j == local_rank or torch.cuda.can_device_access_peer(local_rank, j)
+            for j in range(min(world, torch.cuda.device_count())))
+        transport = "p2p" if world > 1 and uly_n == 1 and peers_ok else "native"
     blk = SkiparseBlock(g, heads, C, batch=1, group=group if world > 1 else None, log=log,
                         device=dev, ulysses_group=uly_group, transport=transport)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
