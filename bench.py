@@ -266,6 +266,10 @@ def run_ours(args, world, rank, local_rank):
         peers_ok = world > 1 and all(
             j == local_rank or torch.cuda.can_device_access_peer(local_rank, j)
             for j in range(min(world, torch.cuda.device_count())))
+        if world > 1:   # every rank must take the same transport
+            ok = torch.tensor([1 if peers_ok else 0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            peers_ok = bool(ok.item())
         transport = "p2p" if world > 1 and uly_n == 1 and peers_ok else "native"
     blk = SkiparseBlock(g, heads, C, batch=1, group=group if world > 1 else None, log=log,
                         device=dev, ulysses_group=uly_group, transport=transport)
