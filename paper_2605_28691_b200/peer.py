@@ -110,12 +110,15 @@ class PeerArena:
         return out.view(table.numel() // out_rows, out_rows, C)
 
     def close(self) -> None:
+        """Collective: unmap the peers' buffers, wait until every rank has, then free our own."""
         if self._own is None:
             return
+        import torch.distributed as dist
         L = _lib.lib()
         torch.cuda.synchronize()
         for p in self._imported:
             L.osp_peer_close(ctypes.c_void_p(p))
+        dist.barrier(group=self.group)
         L.osp_peer_free(ctypes.c_void_p(self._own))
         self._own, self._imported, self._views = None, [], []
 
@@ -126,9 +129,10 @@ _ARENAS: dict = {}
 def shared_arena(group, slot_bytes: int) -> PeerArena:
     """One arena per group, shared by every block (the same shapes repeat down a stack).
     Collective: every rank must call it with the same slot_bytes."""
-    key = id(group)
+    key = group   # the group object itself (held), so a recycled id() can never alias it
     a = _ARENAS.get(key)
-    if a is None or a.slot_bytes < slot_bytes or a.host_sync != (os.environ.get("OSP_PEER_HOST_SYNC") == "1"):
+    if (a is None or a._own is None or a.slot_bytes < slot_bytes
+            or a.host_sync != (os.environ.get("OSP_PEER_HOST_SYNC") == "1")):
         a = PeerArena(group, slot_bytes)
         _ARENAS[key] = a
     return a
