@@ -20,6 +20,12 @@
 
 #include <cstdlib>
 
+// Experiment switches (BwdArgs::flags) are compiled in only with -DOSP_BWD_EXPERIMENTS=1, so the
+// production kernels carry no never-taken branches.
+#ifndef OSP_BWD_EXPERIMENTS
+#define OSP_BWD_EXPERIMENTS 0
+#endif
+
 namespace osp {
 namespace {
 
@@ -395,7 +401,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tc_fence_before();
           mbar_arrive(bar_dqf);
         }
-        if (qg < len && !(a.flags & 1)) {
+        if (qg < len && !((OSP_BWD_EXPERIMENTS ? a.flags : 0) & 1)) {
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             red_add_v4(dst + cc * 32 + j * 4, __uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
@@ -584,7 +590,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       for (int i = 0; i < n_q; ++i) {
         const int st = i % Ly::kStages;
         mbar_wait(bar_qe + st, ((i / Ly::kStages) & 1) ^ 1);
-        if ((a.flags & 64) && i >= 2) {  // experiment 64: no Q/dO reloads (stale tiles, timing only)
+        if (((OSP_BWD_EXPERIMENTS ? a.flags : 0) & 64) && i >= 2) {  // experiment 64: no Q/dO reloads (stale tiles, timing only)
           mbar_arrive(bar_qf + st);
           continue;
         }
@@ -740,7 +746,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       }
       mbar_wait(bar_s, i & 1);
       tc_fence_after();
-      if (a.flags & 2) {  // experiment: synchronisation skeleton only
+      if ((OSP_BWD_EXPERIMENTS ? a.flags : 0) & 2) {  // experiment: synchronisation skeleton only
         tc_fence_before();
         mbar_arrive(bar_p);
         mbar_wait(bar_dp, i & 1);
@@ -855,8 +861,8 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       tmem_wait_ld(v1);
       tc_fence_before();
       mbar_arrive(bar_dqf);
-      if (a.flags & 1) continue;
-      if (a.flags & 32) {  // experiment 32: per-thread vector atomics (the previous scheme)
+      if ((OSP_BWD_EXPERIMENTS ? a.flags : 0) & 1) continue;
+      if ((OSP_BWD_EXPERIMENTS ? a.flags : 0) & 32) {  // experiment 32: per-thread vector atomics (the previous scheme)
         float* base = acc + (static_cast<int64_t>(i) * 16 * D + dcol) * 4;  // q/4 block = i*16
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) red_add_v4_plain(base + j4 * D * 4, v0 + j4 * 4);

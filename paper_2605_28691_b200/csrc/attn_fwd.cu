@@ -63,6 +63,12 @@ __device__ __forceinline__ bool bit_at(const uint32_t* bits, int words, int i) {
   return w < words && ((__ldg(bits + w) >> (i & 31)) & 1u);
 }
 
+// Experiment switches (FwdArgs::flags) are compiled in only with -DOSP_FWD_EXPERIMENTS=1: the
+// softmax loop sits at its register budget, and even never-taken runtime branches cost time.
+#ifndef OSP_FWD_EXPERIMENTS
+#define OSP_FWD_EXPERIMENTS 0
+#endif
+
 template <int D>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -84,6 +90,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int flags = OSP_FWD_EXPERIMENTS ? a.flags : 0;
   const int head = blockIdx.y;
   const int seq = blockIdx.z;
   const int q_row0 = blockIdx.x * 2 * kBM;
@@ -174,7 +181,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int j = 0; j < n_kv; ++j) {
         const int st = j & 1;
         const uint32_t ph = (j >> 1) & 1;
-        if ((a.flags & 8) && j >= 2) {  // experiment 8: no K/V reloads (stale tiles, timing only)
+        if ((flags & 8) && j >= 2) {  // experiment 8: no K/V reloads (stale tiles, timing only)
           mbar_wait(bar_ke + st, ph ^ 1);
           mbar_arrive(bar_kf + st);
           mbar_wait(bar_ve + st, ph ^ 1);
@@ -275,7 +282,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // finishes within the window the other tile's MMAs cover, instead of both running at half
     // speed.  Warpgroup 1 opens the first turn for warpgroup 0.
     const uint32_t my_turn = 2 + t, next_turn = 3 - t;
-    const bool pingpong = !(a.flags & 4);  // experiment 4: no exp-phase serialisation
+    const bool pingpong = !(flags & 4);  // experiment 4: no exp-phase serialisation
     if (t == 1 && pingpong) asm volatile("bar.arrive %0, 256;" ::"r"(2u) : "memory");
 
     float m_used = -INFINITY;
@@ -303,7 +310,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (j + 1 < n_kv) mask_words(j + 1, w_next);
       mbar_wait(bar_s + t, j & 1);
       tc_fence_after();
-      if (a.flags & 2) {
+      if (flags & 2) {
         tc_fence_before();
         mbar_arrive(bar_p + t);
         continue;
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int i = 0; i < 16; ++i) {
             float p0 = fmaf(__uint_as_float(s[cc][2 * i]), c, -ms);
             float p1 = fmaf(__uint_as_float(s[cc][2 * i + 1]), c, -ms);
-            if (!(a.flags & 1)) {
+            if (!(flags & 1)) {
               p0 = ex2(p0);
               p1 = ex2(p1);
             }
