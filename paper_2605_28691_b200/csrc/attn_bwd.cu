@@ -527,9 +527,9 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
                  tDK = tmem + 384;
   const int64_t sh = static_cast<int64_t>(seq) * a.heads + head;
 
-  // register budget (setmaxnreg, total < 64K): control warps 56, compute 176, writers 88
+  // register budget (setmaxnreg, total < 64K): control warps 64, compute 176, writers 88
   if (warp < 4) {
-    regs_dec<56>();
+    regs_dec<64>();
     if (warp == 0 && a.row_index) {
       // -------------------------------------------------------------- TMA producer, gather mode:
       // tile::gather4 of 4 token rows per lane and 64 columns (K, V once; Q, dO per query tile)
