@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
           // dK += dS^T Q with dS^T read from TMEM (TS; written over the consumed dP^T columns)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_ts(mDK, mDP + kk * 8, sdesc_sw128(qb + kk * 2048, 8192, 1024), kIdKV,
+            mma_ts(mDK, mDP + (kk >> 1) * 32 + (kk & 1) * 8, sdesc_sw128(qb + kk * 2048, 8192, 1024), kIdKV,
                    (i > 0 || kk > 0) ? 1u : 0u);
           tc_commit(bar_qe + st);
         }
@@ -802,9 +802,9 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
           *reinterpret_cast<uint4*>(row + phys * 16) =
               make_uint4(pk[ch * 4 + 0], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
         }
-        // both warpgroups must have read dP^T before either overwrites it with dS^T
-        named_bar_sync(1, 256);
-        tmem_st16(tDP + la + half * 16, pk);
+        // dS^T of query half h goes to columns [32h, 32h + 16): inside the dP^T columns this
+        // warpgroup itself read, so neither warpgroup waits for the other
+        tmem_st16(tDP + la + half * 32, pk);
       }
       tmem_wait_st();
       fence_proxy_async_smem();
