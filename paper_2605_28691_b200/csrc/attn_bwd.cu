@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 // tools/mma_rate.cu) is the binding resource, so operands that can live in TMEM do:
 //   TMEM: [0,64) K (A operand of S^T, copied once), [64,128) S^T then P^T (query half h
 //         packed at [64 + 32h, 80 + 32h)),
-//         [128,192) dP^T then dS^T, [192,256) dQ^T, [256,384) dV, [384,512) dK.
+//         [128,192) dP^T then dS^T (half h at +32h), [192,256) dQ^T, [256,384) dV, [384,512) dK.
 //   S^T = K Q^T (TS), dP^T = V dO^T (SS), dV += P^T dO (TS), dK += dS^T Q (TS),
 //   dQ^T_i = K^T dS_i^T (SS, dS^T also staged in smem as the B operand).
 //   dQ^T is drained by four writer warps (thread = d) with 16-byte fp32 vector atomics into a
