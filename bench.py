@@ -355,8 +355,8 @@ def run_ours(args, world, rank, local_rank):
         stream.wait_event(ready[b])
         xin = bufs[b].detach().requires_grad_(True)
         y = blk(xin)
-        # the step's scalar loss <y, gy> as one GEMV pass (fp32 accumulate), read back below
-        loss = torch.mm(y.detach().reshape(1, -1), gy.reshape(-1, 1)).float()
+        # the step's scalar loss <y, gy> as one dot-product pass (fp32 accumulate), read back below
+        loss = torch.dot(y.detach().reshape(-1), gy.reshape(-1)).float()
         y.backward(gy)
         consumed[b].record(stream)
         host_loss[i:i + 1].copy_(loss.detach().view(1), non_blocking=True)
