@@ -37,6 +37,7 @@ CONFIGS = {
     "cfg1": (4, 16, 16, 2, 4, 64, "4x16x16 latent, 4 heads x 64, k=2 (reference CPU case)"),
     "cfg2": (21, 30, 52, 2, 12, 128, "Wan-1.3B shape 12x128 on 480p latent 21x30x52, k=2"),
     "cfg3": (21, 45, 80, 2, 40, 128, "Wan-14B shape 40x128 on 720p latent 21x45x80, k=2"),
+    "cfg3k4": (21, 45, 80, 4, 40, 128, "Wan-14B shape 40x128 on 720p latent 21x45x80, k=4"),
     "cfg5k2": (33, 45, 80, 2, 40, 128, "Wan-14B shape on 129-frame 720p latent 33x45x80, k=2"),
     "cfg5k4": (33, 45, 80, 4, 40, 128, "Wan-14B shape on 129-frame 720p latent 33x45x80, k=4"),
 }
