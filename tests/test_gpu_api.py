@@ -253,11 +253,12 @@ def test_ssp_channel_split_composability(P):
         assert torch.equal(merged, whole.shards[r].tensor.data)
 
 
-def test_block_matches_composed_applications(P):
+@pytest.mark.parametrize("grid", [(2, 10, 12, 2), (1, 10, 12, 3), (1, 17, 20, 4), (2, 16, 16, 4)])
+def test_block_matches_composed_applications(P, grid):
     """SkiparseBlock (steady-state TSA layout) equals two reference-style
-    applications composed through the original layout."""
+    applications composed through the original layout (k = 2, 3, 4; padded and not)."""
     from paper_2605_28691_b200.block import SkiparseBlock
-    g = P.GridShape(2, 10, 12, 2)
+    g = P.GridShape(*grid)
     pg = P.pad_grid(g)
     C, heads = 256, 2
     blk = SkiparseBlock(g, heads, C)
