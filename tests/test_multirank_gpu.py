@@ -84,7 +84,8 @@ def _worker(rank, world, port, grid, transport, q):
 
 @pytest.mark.parametrize("grid,transport", [((2, 10, 12, 2), "native"), ((2, 8, 16, 2), "native"),
                                             ((2, 10, 12, 2), "hif8"), ((2, 10, 12, 2), "p2p"),
-                                            ((2, 8, 16, 2), "p2p"), ((2, 10, 12, 2), "p2p+prologue")])
+                                            ((2, 8, 16, 2), "p2p"), ((2, 10, 12, 2), "p2p+prologue"),
+                                            ((1, 17, 20, 4), "native"), ((1, 17, 20, 4), "p2p")])
 def test_two_rank_block_matches_one_gpu_block(lib, grid, transport):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
