@@ -21,24 +21,31 @@ def _pull(srcs, table, stride):
     return flat[idx]
 
 
-@pytest.mark.parametrize("grid,world", [((2, 10, 12, 2), 2), ((2, 10, 12, 2), 4), ((1, 8, 16, 2), 2),
-                                        ((2, 9, 17, 3), 3)])
+@pytest.mark.parametrize("grid,world,batch", [((2, 10, 12, 2), 2, 1), ((2, 10, 12, 2), 4, 1),
+                                              ((1, 8, 16, 2), 2, 1), ((2, 9, 17, 3), 3, 1),
+                                              ((2, 10, 12, 2), 4, 2), ((1, 9, 17, 3), 9, 2)])
 @pytest.mark.parametrize("padded_gsa", [False, True])
-def test_block_switch_tables_equal_expand_switch_compact(grid, world, padded_gsa):
+def test_block_switch_tables_equal_expand_switch_compact(grid, world, batch, padded_gsa):
     from paper_2605_28691_b200.compact import compact_plan
     from paper_2605_28691_b200.peer import block_switch_moves
     og = O.Grid(*grid)
     pgr = O.padded_grid(og)
     k2 = og.k * og.k
-    L = pgr.seq_len // k2
-    local = k2 // world
+    S = pgr.seq_len
+    L = S // k2
+    local = k2 * batch // world
     LR = local * L
-    vt = torch.from_numpy(O.subseq_mask(og, "tsa"))
-    vg = torch.from_numpy(O.subseq_mask(og, "gsa"))
+    mask = O.pad_mask(og)
+
+    def valid(name):   # validity of every (subsequence, position) slot, rows nested (pattern, b)
+        tab = O.map_table(name, pgr, batch)
+        return torch.from_numpy(mask[tab.reshape(-1) % S].reshape(k2 * batch, L))
+
+    vt, vg = valid("orig_to_tsa"), valid("orig_to_gsa")
     pts = [compact_plan(vt[j * local:(j + 1) * local]) for j in range(world)]
     pgs = [compact_plan(vg[j * local:(j + 1) * local]) for j in range(world)]
-    t2g = torch.from_numpy(O.map_table("tsa_to_gsa", pgr, 1).reshape(-1))
-    g2t = torch.from_numpy(O.map_table("gsa_to_tsa", pgr, 1).reshape(-1))
+    t2g = torch.from_numpy(O.map_table("tsa_to_gsa", pgr, batch).reshape(-1))
+    g2t = torch.from_numpy(O.map_table("gsa_to_tsa", pgr, batch).reshape(-1))
     C = 5
     gen = torch.Generator().manual_seed(7)
     # compact attention outputs, junk beyond each subsequence's length: it must never be read
