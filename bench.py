@@ -259,19 +259,12 @@ def run_ours(args, world, rank, local_rank):
         groups = [dist.new_group(list(range(i * ssp_n, (i + 1) * ssp_n))) for i in range(dp)]
         group = groups[rank // ssp_n]
     log = CommLog()
-    # the SSP switch: one pull over NVLink peer memory (K7) when SSP alone shards the latent;
-    # NCCL all-to-all around the Ulysses groups
+    # the SSP switch: pack (K4) -> one NCCL all-to-all -> unpack, overlapped with attention in
+    # head chunks.  The one-pull peer-memory switch (K7, --transport p2p) stays opt-in: its device
+    # barrier has not yet run across real GPUs, and CUDA-IPC handles only open on one host.
     transport = args.transport
     if transport == "auto":
-        # p2p needs every rank's GPU to map every peer's memory (one NVLink / NVSwitch domain)
-        peers_ok = world > 1 and all(
-            j == local_rank or torch.cuda.can_device_access_peer(local_rank, j)
-            for j in range(min(world, torch.cuda.device_count())))
-        if world > 1:   # every rank must take the same transport
-            ok = torch.tensor([1 if peers_ok else 0], device=dev)
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-            peers_ok = bool(ok.item())
-        transport = "p2p" if world > 1 and uly_n == 1 and peers_ok else "native"
+        transport = "native"
     blk = SkiparseBlock(g, heads, C, batch=1, group=group if world > 1 else None, log=log,
                         device=dev, ulysses_group=uly_group, transport=transport)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -446,7 +439,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=2048)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--transport", default="auto", choices=["auto", "native", "hif8", "p2p"],
-                    help="SSP switch transport for N > 1 (auto: p2p pull unless Ulysses is on)")
+                    help="SSP switch transport for N > 1 (auto = native NCCL; p2p = K7 peer pull, one host)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -474,6 +467,8 @@ def main():
     finally:
         if world > 1:
             import torch.distributed as dist
+            from paper_2605_28691_b200.peer import close_arenas
+            close_arenas()
             dist.destroy_process_group()
 
 

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define OSP_ABI_VERSION 1
+#define OSP_ABI_VERSION 2
 
 enum osp_status {
   OSP_OK = 0,
@@ -226,6 +226,11 @@ int osp_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, int
  *   osp_peer_barrier: flag_blocks = host array of n device pointers, rank j's uint32[n] flag
  *                    block; publishes `epoch` to slot `rank` of every block and waits until every
  *                    slot of this rank's block reached it (epochs increase by one per barrier).
+ *                    timeout_ms > 0 bounds the wait: a rank that never arrives makes the kernel
+ *                    write (1 + that rank) into *status (host-mapped pinned memory, first
+ *                    timeout wins) and EXIT instead of trapping, so the context survives and the
+ *                    host raises CollectiveError when it reads the word (status may be NULL:
+ *                    then the kernel just exits).
  *   osp_peer_gather: dst[i] = row (table[i] % stride_rows) of srcs[table[i] / stride_rows]
  *                    (srcs = host array of n_src device pointers, local or peer-mapped);
  *                    table[i] < 0 gives a zero row.  table is a device int64 array of n_rows.
@@ -235,7 +240,8 @@ int osp_peer_free(void* ptr);
 int osp_peer_export(void* ptr, uint8_t* handle64);
 int osp_peer_import(const uint8_t* handle64, void** ptr);
 int osp_peer_close(void* ptr);
-int osp_peer_barrier(const void* const* flag_blocks, int rank, int n, uint32_t epoch, void* stream);
+int osp_peer_barrier(const void* const* flag_blocks, int rank, int n, uint32_t epoch,
+                     int64_t timeout_ms, int* status, void* stream);
 int osp_peer_gather(const void* const* srcs, int n_src, int64_t stride_rows, const int64_t* table,
                     int64_t n_rows, void* dst, int64_t row_bytes, void* stream);
 

@@ -152,6 +152,10 @@ class SkiparseBlock:
             elif self.uly > 1 or not compact:
                 raise ValueError("the p2p switch needs compaction and no Ulysses group")
             else:
+                from .peer import same_host
+                if not same_host(group):
+                    raise ValueError("the p2p switch maps peers' memory through CUDA IPC: every "
+                                     "rank of the SSP group must be on one host")
                 from .compact import compact_plan
                 from .peer import block_switch_moves, shared_arena
                 rng = [(j * self.local_rows, (j + 1) * self.local_rows) for j in range(self.world)]

@@ -428,8 +428,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 //         [128,192) dP^T then dS^T (half h at +32h), [192,256) dQ^T, [256,384) dV, [384,512) dK.
 //   S^T = K Q^T (TS), dP^T = V dO^T (SS), dV += P^T dO (TS), dK += dS^T Q (TS),
 //   dQ^T_i = K^T dS_i^T (SS, dS^T also staged in smem as the B operand).
-//   dQ^T is drained by four writer warps (thread = d) with 16-byte fp32 vector atomics into a
-//   (seq*head, q/4, d, q%4) accumulator so a warp instruction covers 512 contiguous bytes.
+//   dQ^T is drained by four writer warps (thread = d): tcgen05.ld into registers, staged in
+//   shared memory in the accumulator's (q/4, d, q%4) fp32 layout, and added into the
+//   (seq*head, q/4, d, q%4) L2 accumulator by ONE cp.reduce.async.bulk of 32 KB per tile.
 //   Eight compute warps (thread = key row) split each tile's 64 query columns.
 //   MMA order: S_0, dP_0, then per i: dV_i, S_{i+1}, dK_i, dQ^T_i, dP_{i+1}.
 struct BwdV2Layout {
@@ -1105,18 +1106,14 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     const char* f = getenv("OSP_BWD_FLAGS");
     a.flags = f ? atoi(f) : 0;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    rc = check_cuda(cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         BwdLayout<D>::kSmem),
-                    "cudaFuncSetAttribute(attn_bwd)");
-    if (rc != kOk) return rc;
-    rc = check_cuda(cudaFuncSetAttribute(attn_bwd_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         BwdV2Layout::kSmemX),
-                    "cudaFuncSetAttribute(attn_bwd_v2)");
-    if (rc != kOk) return rc;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done_v1{0}, attr_done_v2{0};
+  if constexpr (D == 128)
+    rc = set_smem_attr(reinterpret_cast<const void*>(attn_bwd_v2_kernel), BwdV2Layout::kSmemX, attr_done_v2,
+                       "cudaFuncSetAttribute(attn_bwd_v2)");
+  else
+    rc = set_smem_attr(reinterpret_cast<const void*>(attn_bwd_kernel<D>), BwdLayout<D>::kSmem, attr_done_v1,
+                       "cudaFuncSetAttribute(attn_bwd)");
+  if (rc != kOk) return rc;
   dim3 grid(static_cast<unsigned>(seq_pad / 128), static_cast<unsigned>(s.heads),
             static_cast<unsigned>(s.n_seq));
   if constexpr (D == 128) {

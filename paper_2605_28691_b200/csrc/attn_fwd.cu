@@ -495,15 +495,10 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
   }
   const int n_qt = static_cast<int>((s.seq_len + kBM - 1) / kBM);
   dim3 grid((n_qt + 1) / 2, static_cast<unsigned>(s.heads), static_cast<unsigned>(s.n_seq));
-  static bool attr_set = false;
-  if (!attr_set) {
-    int rc = check_cuda(cudaFuncSetAttribute(attn_fwd_kernel<D>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             FwdLayout<D>::kSmem),
-                        "cudaFuncSetAttribute(attn_fwd)");
-    if (rc != kOk) return rc;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  st = set_smem_attr(reinterpret_cast<const void*>(attn_fwd_kernel<D>), FwdLayout<D>::kSmem, attr_done,
+                     "cudaFuncSetAttribute(attn_fwd)");
+  if (st != kOk) return st;
   attn_fwd_kernel<D><<<grid, kFwdThreads, FwdLayout<D>::kSmem, stream>>>(mq, mk, mv, a);
   return check_cuda(cudaGetLastError(), "attn_fwd_kernel launch");
 }

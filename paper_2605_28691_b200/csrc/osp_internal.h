@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 namespace osp {
@@ -27,6 +28,13 @@ enum Status : int {
 };
 
 int check_cuda(cudaError_t e, const char* what);
+
+// Raise a kernel's dynamic shared-memory limit on the CURRENT device, once per (kernel, device).
+// The attribute is per device context, so a process that drives several GPUs (the survey's
+// single-process multi-device path) must set it on each; `done` is the call site's per-device
+// bitmask (one bit per device ordinal < 64).  Concurrent first calls may both set the attribute,
+// which is idempotent.
+int set_smem_attr(const void* kernel, int bytes, std::atomic<uint64_t>& done, const char* what);
 
 // Build a 3-D bf16 TMA descriptor over a (n_seq, rows, cols) row-strided matrix with a
 // (64 x box_rows x 1) box and 128-byte swizzle.

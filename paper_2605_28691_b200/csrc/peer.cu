@@ -42,7 +42,10 @@ __device__ __forceinline__ uint64_t global_ns() {
 }
 
 // flags.p[j] = rank j's flag block (uint32[n]); slot i of a block is written by rank i only.
-__global__ void peer_barrier_kernel(const PeerPtrs flags, int rank, int n, uint32_t epoch) {
+// A rank that has not arrived after timeout_ns is reported through *status (1 + rank, first
+// timeout wins) and the kernel returns: no __trap, so the context survives for a diagnosis.
+__global__ void peer_barrier_kernel(const PeerPtrs flags, int rank, int n, uint32_t epoch,
+                                    uint64_t timeout_ns, int* status) {
   const int t = threadIdx.x;
   if (t >= n) return;
   __threadfence_system();
@@ -51,7 +54,13 @@ __global__ void peer_barrier_kernel(const PeerPtrs flags, int rank, int n, uint3
   const uint64_t t0 = global_ns();
   // epochs only grow; compare modulo 2^32
   while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
-    if (global_ns() - t0 > 60ull * 1000000000ull) __trap();  // a rank never arrived
+    if (global_ns() - t0 > timeout_ns) {  // rank t never arrived
+      if (status) {
+        atomicCAS_system(status, 0, 1 + t);
+        __threadfence_system();
+      }
+      return;
+    }
   }
 }
 
@@ -153,7 +162,8 @@ int osp_peer_import(const uint8_t* handle64, void** ptr) {
 
 int osp_peer_close(void* ptr) { return check_cuda(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle"); }
 
-int osp_peer_barrier(const void* const* flag_blocks, int rank, int n, uint32_t epoch, void* stream) {
+int osp_peer_barrier(const void* const* flag_blocks, int rank, int n, uint32_t epoch,
+                     int64_t timeout_ms, int* status, void* stream) {
   PeerPtrs pp;
   int rc = fill_ptrs(pp, flag_blocks, n);
   if (rc != kOk) return rc;
@@ -161,7 +171,10 @@ int osp_peer_barrier(const void* const* flag_blocks, int rank, int n, uint32_t e
     set_error("rank out of range");
     return kValue;
   }
-  peer_barrier_kernel<<<1, 32 * ((n + 31) / 32), 0, peer_stream(stream)>>>(pp, rank, n, epoch);
+  const uint64_t timeout_ns =
+      timeout_ms > 0 ? static_cast<uint64_t>(timeout_ms) * 1000000ull : 60ull * 1000000000ull;
+  peer_barrier_kernel<<<1, 32 * ((n + 31) / 32), 0, peer_stream(stream)>>>(pp, rank, n, epoch,
+                                                                          timeout_ns, status);
   return check_cuda(cudaGetLastError(), "peer_barrier launch");
 }
 

@@ -419,18 +419,13 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   CUtensorMap ma, mb;
   if ((rc = make_tmap_bf16_3d(&ma, x, chan, rows, 1, chan, kPBM)) != kOk) return rc;
   if ((rc = make_tmap_bf16_3d(&mb, w_t, chan, n, 1, chan, kPBN / 2)) != kOk) return rc;  // W half
-  static bool attr_set = false;
-  if (!attr_set) {
-    rc = check_cuda(cudaFuncSetAttribute(qkv_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         ProjLayout::kSmem),
-                    "cudaFuncSetAttribute(qkv_gemm)");
-    if (rc != kOk) return rc;
-    rc = check_cuda(cudaFuncSetAttribute(qkv_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Proj2Layout::kSmem),
-                    "cudaFuncSetAttribute(qkv_gemm pair)");
-    if (rc != kOk) return rc;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done_1{0}, attr_done_2{0};
+  rc = set_smem_attr(reinterpret_cast<const void*>(qkv_gemm_kernel<false>), ProjLayout::kSmem, attr_done_1,
+                     "cudaFuncSetAttribute(qkv_gemm)");
+  if (rc != kOk) return rc;
+  rc = set_smem_attr(reinterpret_cast<const void*>(qkv_gemm_kernel<true>), Proj2Layout::kSmem, attr_done_2,
+                     "cudaFuncSetAttribute(qkv_gemm pair)");
+  if (rc != kOk) return rc;
   {
     const char* be = getenv("OSP_PROJ_BAND");
     a.band = be ? atoi(be) : 12;  // measured best at cfg3 (tools/bench_proj.py, OSP_PROJ_BAND)

@@ -133,12 +133,15 @@ def peer_gather(src_ptrs, stride_rows: int, table: torch.Tensor, out: torch.Tens
     return out
 
 
-def peer_barrier(flag_ptrs, rank: int, epoch: int, device=None) -> None:
-    """K7: device-side flag barrier over the peers' flag blocks (see include/osp_skiparse.h)."""
+def peer_barrier(flag_ptrs, rank: int, epoch: int, device=None, timeout_ms: int = 0,
+                 status: torch.Tensor | None = None) -> None:
+    """K7: device-side flag barrier over the peers' flag blocks (see include/osp_skiparse.h).
+    status: pinned host int32 word the kernel sets to 1 + the missing rank on timeout."""
     L = _lib.lib()
     arr = _ptr_array(flag_ptrs)
     _lib.check(STATS.run('peer_barrier', 1, lambda: L.osp_peer_barrier(
-        arr, rank, len(flag_ptrs), epoch & 0xFFFFFFFF, _lib.stream_ptr(device))))
+        arr, rank, len(flag_ptrs), epoch & 0xFFFFFFFF, int(timeout_ms), _lib.ptr(status),
+        _lib.stream_ptr(device))))
 
 
 def invert_index(index: torch.Tensor) -> torch.Tensor:

@@ -29,8 +29,8 @@ import torch
 
 from . import _lib, kernels
 
-__all__ = ["PeerArena", "PeerMove", "peer_move", "shared_arena", "peer_switch", "block_switch_moves",
-           "padded_switch_moves"]
+__all__ = ["PeerArena", "PeerMove", "peer_move", "shared_arena", "close_arenas", "same_host", "peer_switch",
+           "block_switch_moves", "padded_switch_moves"]
 
 
 class _Mem:
@@ -43,29 +43,57 @@ def _round(n: int, a: int = 256) -> int:
     return (n + a - 1) // a * a
 
 
+def _timeout_ms() -> int:
+    return int(float(os.environ.get("OSP_PEER_TIMEOUT_S", "60")) * 1000)
+
+
+def same_host(group) -> bool:
+    """True when every rank of `group` runs on this host (CUDA-IPC handles only open locally).
+    Collective over `group`."""
+    import socket
+
+    import torch.distributed as dist
+    names = [None] * dist.get_world_size(group)
+    dist.all_gather_object(names, socket.gethostname(), group=group)
+    return len(set(names)) == 1
+
+
 class PeerArena:
     """One CUDA-IPC buffer per rank of `group`: a flag block (uint32 per rank) followed by
-    `slots` source slots of `slot_bytes`; every rank holds every peer's base address."""
+    `slots` source slots of `slot_bytes`; every rank holds every peer's base address.
+
+    The device barrier is bounded by OSP_PEER_TIMEOUT_S (default 60 s): a rank that never
+    arrives is reported through a pinned host status word (no __trap, the context survives) and
+    the next barrier / close() raises CollectiveError naming it."""
 
     def __init__(self, group, slot_bytes: int, slots: int = 2, host_sync: bool | None = None):
         import torch.distributed as dist
-        L = _lib.lib()
         self.group = group
         self.n = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.host_sync = (os.environ.get("OSP_PEER_HOST_SYNC") == "1") if host_sync is None else host_sync
         self.flag_bytes = _round(4 * self.n)
-        self.slot_bytes = _round(max(slot_bytes, 1))
         self.slots = slots
         self.device = torch.device("cuda", torch.cuda.current_device())
-        total = self.flag_bytes + slots * self.slot_bytes
+        self.status = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self.timeout_ms = _timeout_ms()
+        self._own = None
+        self._imported = []
+        self._map(slot_bytes)
+
+    def _map(self, slot_bytes: int) -> None:
+        """Collective: allocate, export and import every rank's buffer."""
+        import torch.distributed as dist
+        L = _lib.lib()
+        self.slot_bytes = _round(max(slot_bytes, 1))
+        total = self.flag_bytes + self.slots * self.slot_bytes
         base = ctypes.c_void_p()
         _lib.check(L.osp_peer_alloc(total, ctypes.byref(base)))
         self._own = base.value
         handle = (ctypes.c_uint8 * 64)()
         _lib.check(L.osp_peer_export(ctypes.c_void_p(self._own), handle))
         handles = [None] * self.n
-        dist.all_gather_object(handles, bytes(handle), group=group)
+        dist.all_gather_object(handles, bytes(handle), group=self.group)
         self._imported = []
         self.bases = []
         for j, h in enumerate(handles):
@@ -80,11 +108,28 @@ class PeerArena:
         self.turn = 0
         self._views = [torch.as_tensor(_Mem(self._own + self.flag_bytes + s * self.slot_bytes,
                                             self.slot_bytes), device=self.device)
-                       for s in range(slots)]
+                       for s in range(self.slots)]
+
+    def ensure(self, slot_bytes: int) -> "PeerArena":
+        """Collective: grow the slots in place (old mappings are released first), so every block
+        sharing this arena sees the larger buffer and nothing leaks."""
+        if self._own is None or self.slot_bytes < slot_bytes:
+            self._unmap()
+            self._map(slot_bytes)
+        return self
 
     # ------------------------------------------------------------------ pieces
     def slot_ptrs(self, s: int) -> list[int]:
         return [b + self.flag_bytes + s * self.slot_bytes for b in self.bases]
+
+    def check(self) -> None:
+        """Raise CollectiveError if an earlier device barrier timed out (reads the pinned
+        status word the barrier kernel writes; no device synchronisation)."""
+        v = int(self.status[0])
+        if v:
+            from .errors import CollectiveError
+            raise CollectiveError(f"peer barrier: rank {v - 1} of {self.n} did not arrive within "
+                                  f"{self.timeout_ms / 1000:g} s (OSP_PEER_TIMEOUT_S)")
 
     def barrier(self) -> None:
         if self.host_sync:
@@ -92,10 +137,13 @@ class PeerArena:
             torch.cuda.synchronize()
             dist.barrier(group=self.group)
             return
+        self.check()
         self.epoch += 1
-        kernels.peer_barrier(self.bases, self.rank, self.epoch, self.device)
+        kernels.peer_barrier(self.bases, self.rank, self.epoch, self.device, self.timeout_ms,
+                             self.status)
 
-    def move(self, x: torch.Tensor, table: torch.Tensor, stride: int, out_rows: int) -> torch.Tensor:
+    def move(self, x: torch.Tensor, table: torch.Tensor, stride: int, out_rows: int,
+             col0: int = 0, out: torch.Tensor | None = None) -> torch.Tensor:
         """Publish x's rows in the next slot, barrier, pull `table` from every rank's slot."""
         C = x.shape[-1]
         nb = x.numel() * x.element_size()
@@ -105,12 +153,12 @@ class PeerArena:
         self.turn = (self.turn + 1) % self.slots
         self._views[s][:nb].view(x.dtype).view(x.shape).copy_(x)
         self.barrier()
-        out = torch.empty((table.numel(), C), dtype=x.dtype, device=x.device)
+        if out is None:
+            out = torch.empty((table.numel(), C), dtype=x.dtype, device=x.device)
         kernels.peer_gather(self.slot_ptrs(s), stride, table, out)
         return out.view(table.numel() // out_rows, out_rows, C)
 
-    def close(self) -> None:
-        """Collective: unmap the peers' buffers, wait until every rank has, then free our own."""
+    def _unmap(self) -> None:
         if self._own is None:
             return
         import torch.distributed as dist
@@ -122,20 +170,38 @@ class PeerArena:
         L.osp_peer_free(ctypes.c_void_p(self._own))
         self._own, self._imported, self._views = None, [], []
 
+    def close(self) -> None:
+        """Collective: unmap the peers' buffers, wait until every rank has, then free our own."""
+        if self._own is None:
+            return
+        self._unmap()
+        self.check()
+
 
 _ARENAS: dict = {}
 
 
 def shared_arena(group, slot_bytes: int) -> PeerArena:
-    """One arena per group, shared by every block (the same shapes repeat down a stack).
-    Collective: every rank must call it with the same slot_bytes."""
+    """One arena per group, shared by every block (the same shapes repeat down a stack); a block
+    that needs larger slots grows the shared arena in place.  Collective: every rank must call
+    it with the same slot_bytes."""
     key = group   # the group object itself (held), so a recycled id() can never alias it
     a = _ARENAS.get(key)
-    if (a is None or a._own is None or a.slot_bytes < slot_bytes
-            or a.host_sync != (os.environ.get("OSP_PEER_HOST_SYNC") == "1")):
+    host_sync = os.environ.get("OSP_PEER_HOST_SYNC") == "1"
+    if a is not None and a.host_sync != host_sync:
+        a.close()
+        a = None
+    if a is None:
         a = PeerArena(group, slot_bytes)
         _ARENAS[key] = a
-    return a
+    return a.ensure(slot_bytes)
+
+
+def close_arenas() -> None:
+    """Collective teardown of every shared arena (call before destroy_process_group)."""
+    while _ARENAS:
+        _, a = _ARENAS.popitem()
+        a.close()
 
 
 @dataclass(frozen=True)

@@ -31,7 +31,7 @@ def test_header_and_binding_agree():
 def test_library_exports_every_symbol(cdll):
     for name in _header_functions():
         assert hasattr(cdll, name), name
-    assert cdll.osp_abi_version() == 1
+    assert cdll.osp_abi_version() == 2
 
 
 def test_library_is_sm100a_only(cdll):

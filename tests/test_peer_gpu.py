@@ -73,6 +73,63 @@ def test_peer_arena_single_rank_round_trip(lib):
                 assert torch.equal(y.view(96, 40), x.view(96, 40)[perm])
                 back = arena.move(y, mv.inv, mv.inv_stride, mv.in_rows)
                 assert torch.equal(back, x)
+            old = arena.slot_bytes
+            arena.ensure(4 * old)        # grows in place: old mappings released, same object
+            assert arena.slot_bytes >= 4 * old
+            y = arena.move(x, mv.table, mv.stride, mv.out_rows)
+            assert torch.equal(y.view(96, 40), x.view(96, 40)[perm])
+            arena.status[0] = 2          # as written by a timed-out device barrier
+            from paper_2605_28691_b200.errors import CollectiveError
+            with pytest.raises(CollectiveError):
+                arena.check()
+            arena.status[0] = 0
             arena.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_peer_barrier_two_ranks_on_two_streams(lib):
+    """The device barrier protocol with both ranks live: rank r's copy -> barrier -> pull runs on
+    its own stream of one GPU, so rank 0's barrier kernel really spins until rank 1's publishes
+    (no host_sync).  A lost rank would end in the bounded timeout, not a hang."""
+    from paper_2605_28691_b200 import kernels
+    n, rows, chan = 2, 300, 256
+    flags = [torch.zeros(n, dtype=torch.int32, device="cuda") for _ in range(n)]
+    slots = [torch.zeros(rows, chan, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+    status = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+    streams = [torch.cuda.Stream() for _ in range(n)]
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    tables = [torch.randint(0, n * rows, (rows,), generator=gen, device="cuda") for _ in range(n)]
+    torch.cuda.synchronize()
+    for epoch in (1, 2, 3):
+        src = [torch.randn(rows, chan, generator=gen, device="cuda").to(torch.bfloat16) for _ in range(n)]
+        outs = [torch.empty(rows, chan, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+        torch.cuda.synchronize()
+        for r in range(n):        # rank 0's barrier is enqueued before rank 1 has arrived
+            with torch.cuda.stream(streams[r]):
+                slots[r].copy_(src[r])
+                kernels.peer_barrier([f.data_ptr() for f in flags], r, epoch, timeout_ms=20000,
+                                     status=status)
+                kernels.peer_gather([s.data_ptr() for s in slots], rows, tables[r], outs[r])
+        torch.cuda.synchronize()
+        assert int(status[0]) == 0
+        flat = torch.cat(src)
+        for r in range(n):
+            assert torch.equal(outs[r], flat[tables[r]])
+            for j in range(n):
+                assert int(flags[j][r]) == epoch
+
+
+def test_peer_barrier_timeout_reports_missing_rank(lib):
+    """A rank that never arrives: the barrier exits after the timeout with 1 + that rank in the
+    status word (no __trap, the context stays usable) and PeerArena.check raises."""
+    from paper_2605_28691_b200 import kernels
+    n, rank = 3, 0
+    flags = [torch.zeros(n, dtype=torch.int32, device="cuda") for _ in range(n)]
+    flags[rank][1] = 1                 # rank 1 arrived, rank 2 never does
+    status = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+    kernels.peer_barrier([f.data_ptr() for f in flags], rank, 1, timeout_ms=200, status=status)
+    torch.cuda.synchronize()
+    assert int(status[0]) == 1 + 2
+    x = torch.ones(4, device="cuda")
+    assert float((x * 2).sum()) == 8.0   # context still alive
