@@ -48,3 +48,22 @@ def lib():
         pytest.skip("no CUDA device")
     from paper_2605_28691_b200 import _lib
     return _lib.lib()
+
+
+# ---- parity report: tests record max-abs / relative-L2 errors per tensor; with OSP_PARITY_OUT set
+# the session writes them as JSON (profiles/rNN_parity.json is a committed copy of one run)
+PARITY: dict = {}
+
+
+@pytest.fixture(scope="session")
+def parity_record():
+    def rec(case: str, entry: dict):
+        PARITY[case] = entry
+    return rec
+
+
+def pytest_sessionfinish(session, exitstatus):
+    out = os.environ.get("OSP_PARITY_OUT")
+    if out and PARITY:
+        Path(out).parent.mkdir(parents=True, exist_ok=True)
+        Path(out).write_text(json.dumps(PARITY, indent=1, sort_keys=True))
