@@ -114,56 +114,90 @@ def _cpu_slice(args):
     return time.perf_counter() - t0
 
 
-def cpu_oracle_rate(cfg, workers: int, L_sample: int = 2048, reps: int = 1):
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def cpu_oracle_rate(cfg, workers: int, sizes=(2048, 4096, 8192), reps: int = 1):
     """Time the CPU oracle (a port of the reference's float64 numpy dense_attention,
-    attention.py:47-67, single-threaded einsum) on (subsequence, head) slices of
-    length L_sample, `workers` slices in parallel, and extrapolate by L^2 to the
-    full block (2 applications x k^2 x heads slices of the padded length; backward
-    = 2.5 x forward since the reference has none)."""
+    attention.py:47-67, single-threaded einsum) on (subsequence, head) slices at several lengths
+    L_s (`workers` slices in parallel per length), fit t(L) = a * L^p through the per-slice times
+    (log-log least squares; p = 2 with one size) and extrapolate to the full block: 2 applications
+    x k^2 x heads slices of the padded length, backward = 2.5 x forward (the reference has none)."""
+    import math as _m
     T, H, W, k, heads, d, _ = CONFIGS[cfg]
     k2 = k * k
     Hp, Wp = -(-H // k2) * k2, -(-W // k2) * k2
     L = T * Hp * Wp // k2
-    Ls = min(L_sample, L)
-    t0 = time.perf_counter()
-    if workers > 1:
-        import multiprocessing as mp
-        with mp.get_context("fork").Pool(workers) as pool:
-            per = pool.map(_cpu_slice, [(Ls, d, i) for i in range(workers * reps)])
+    sizes = sorted({min(int(s_), L) for s_ in sizes})
+    per_slice, wall_total = {}, 0.0
+    for Ls in sizes:
+        t0 = time.perf_counter()
+        if workers > 1:
+            import multiprocessing as mp
+            with mp.get_context("fork").Pool(workers) as pool:
+                per = pool.map(_cpu_slice, [(Ls, d, i) for i in range(workers * reps)])
+        else:
+            per = [_cpu_slice((Ls, d, i)) for i in range(reps)]
+        wall = time.perf_counter() - t0
+        wall_total += wall
+        per_slice[Ls] = wall / len(per)          # effective seconds per slice on `workers` cores
+    xs = [_m.log(x) for x in sizes]
+    ys = [_m.log(per_slice[x]) for x in sizes]
+    if len(sizes) > 1:
+        mx, my = sum(xs) / len(xs), sum(ys) / len(ys)
+        p = sum((a - mx) * (b - my) for a, b in zip(xs, ys)) / sum((a - mx) ** 2 for a in xs)
+        la = my - p * mx
     else:
-        per = [_cpu_slice((Ls, d, i)) for i in range(reps)]
-    wall = time.perf_counter() - t0
-    slices_per_s = len(per) / wall
+        p, la = 2.0, ys[0] - 2.0 * xs[0]
+    t_full = _m.exp(la + p * _m.log(L))         # seconds per full-length slice
     n_slices = 2 * k2 * heads  # per block (batch 1)
-    sec_block_fwd = n_slices * (L / Ls) ** 2 / slices_per_s
-    sec_block = 3.5 * sec_block_fwd
+    sec_block = 3.5 * n_slices * t_full
     tokens = T * H * W
     return {"value": tokens / sec_block, "unit": "tokens/s", "cores": workers,
-            "sample": (f"{len(per)} float64 dense_attention slices of L={Ls}, d={d} in {wall:.2f} s "
-                       f"on {workers} process(es); extrapolated by (L/{Ls})^2 to L={L}, x{n_slices} "
-                       f"slices/block, bwd=2.5x fwd (reference has no backward)"),
-            "wall_s": wall}
+            "sample": (f"float64 dense_attention (d={d}) slices at L={sizes} ({workers * reps} per length "
+                       f"on {workers} process(es), {wall_total:.1f} s); fit t = a*L^{p:.2f}, extrapolated "
+                       f"to L={L} x{n_slices} slices/block, bwd = 2.5x fwd (the reference has no "
+                       f"backward); host CPU: {cpu_model()}, os.cpu_count() = {os.cpu_count()}"),
+            "wall_s": wall_total, "fit_exponent": p, "per_slice_s": per_slice,
+            "extrapolated_block_s": sec_block}
 
 
 def run_reference(args, world, rank):
+    """The reference arm: the reference's CPU path (the oracle port of its float64 numpy
+    dense_attention; /root/reference is not on the GPU box) on the host cores, one process per
+    core.  Each step is a bounded sample (slices at two lengths on every core); `value` is the
+    full-block tokens/s extrapolated from the fit, `ms_per_step` the measured wall time of one
+    sampled step."""
     if rank != 0:
         return
     import numpy as np  # noqa: F401
     cores = os.cpu_count() or 1
     T, H, W, k, heads, d, desc = CONFIGS[args.config]
     rates = []
-    for _ in range(args.warmup if args.warmup < 2 else 1):
-        cpu_oracle_rate(args.config, cores, 1024)
+    for _ in range(args.warmup):
+        cpu_oracle_rate(args.config, cores, (512,))
+    t0 = time.perf_counter()
     for _ in range(args.steps):
-        rates.append(cpu_oracle_rate(args.config, cores, args.cpu_sample))
+        rates.append(cpu_oracle_rate(args.config, cores, (args.cpu_sample, 2 * args.cpu_sample)))
+    wall_ms = 1000.0 * (time.perf_counter() - t0) / max(args.steps, 1)
     val = statistics.median(r["value"] for r in rates)
-    tokens = T * H * W
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * tokens / val, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": wall_ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "description": desc, "grid": [T, H, W], "k": k,
                        "heads": heads, "head_dim": d, "global_batch": 1},
+            "note": ("ms_per_step is the measured wall time of one bounded sample step; value is the "
+                     "full block's tokens/s extrapolated from it (extrapolated_block_s per block)"),
+            "extrapolated_block_s": statistics.median(r["extrapolated_block_s"] for r in rates),
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": rates[-1]["sample"]},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0,
@@ -231,6 +265,92 @@ def _comm_summary(log, steps: int) -> dict:
             "ulysses_bytes_per_rank_per_step": sum(e.bytes_per_rank for e in uly_ev) // steps}
 
 
+def _parity_summary(cfg: str):
+    """Block parity errors recorded by tests/test_block_parity_gpu.py (committed copy in
+    profiles/rNN_parity.json, newest round first) for this config."""
+    import glob
+    files = sorted(glob.glob(str(ROOT / "profiles" / "r*_parity.json")))
+    for f in reversed(files):
+        d = json.loads(Path(f).read_text())
+        e = d.get(f"block_{cfg}")
+        if e:
+            return {"source": Path(f).name, "rule": e.get("rule"),
+                    **{t: {k_: e[t][k_] for k_ in ("max_abs", "rel_l2", "budget_max_abs", "budget_rel_l2", "pass")}
+                       for t in ("y", "dx") if t in e}}
+    return None
+
+
+def sdpa_comparator(heads: int, d: int, L: int, n_seq: int, dev, reps: int = 3) -> dict:
+    """Same-box anchors for the attention kernels: K2/K3 and torch SDPA backends (cuDNN, and
+    flash when it runs on sm_100) on one application's shape -- n_seq subsequences x heads x L
+    x d, no mask, bf16 -- timed with CUDA events (median of `reps` after a warm-up)."""
+    import math as _m
+
+    import torch
+    import torch.nn.functional as F
+    from paper_2605_28691_b200 import kernels
+    C = heads * d
+    gen = torch.Generator(device=dev).manual_seed(5)
+    qkv = torch.randn(n_seq, L, 3 * C, generator=gen, device=dev).to(torch.bfloat16)
+    do = torch.randn(n_seq, L, C, generator=gen, device=dev).to(torch.bfloat16)
+    fl = 4.0 * n_seq * heads * L * L * d
+    res = {"shape": {"n_seq": n_seq, "heads": heads, "L": L, "head_dim": d}, "fwd_tflop": fl / 1e12}
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    q, k, v = qkv[..., :C], qkv[..., C:2 * C], qkv[..., 2 * C:]
+    sc = 1.0 / _m.sqrt(d)
+    box = {}
+
+    def ours_fwd():
+        box["o"], box["lse"] = kernels.attn_fwd(q, k, v, heads, d, None, False, sc)
+
+    def ours_bwd():
+        kernels.attn_bwd(q, k, v, box["o"], do, box["lse"], heads, d, None, False, sc)
+
+    f_ms = timed(ours_fwd)
+    b_ms = timed(ours_bwd)
+    res["osp_k2_k3"] = {"fwd_ms": f_ms, "bwd_ms": b_ms, "fwd_tflops": fl / f_ms / 1e9,
+                        "bwd_tflops": 2.5 * fl / b_ms / 1e9}
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+    except ImportError:
+        return res
+    # SDPA wants (B, H, L, d): views of the same (n, L, H, d) memory
+    qs, ks, vs = (t.reshape(n_seq, L, heads, d).transpose(1, 2) for t in (q, k, v))
+    dos = do.reshape(n_seq, L, heads, d).transpose(1, 2)
+    for name, be in (("cudnn_sdpa", SDPBackend.CUDNN_ATTENTION), ("flash_sdpa", SDPBackend.FLASH_ATTENTION)):
+        try:
+            ql, kl, vl = (t.detach().requires_grad_(True) for t in (qs, ks, vs))
+
+            def fwd():
+                with sdpa_kernel(be):
+                    box["y"] = F.scaled_dot_product_attention(ql, kl, vl)
+
+            def bwd():
+                torch.autograd.grad(box["y"], (ql, kl, vl), dos, retain_graph=True)
+
+            fm = timed(fwd)
+            fwd()
+            bm = timed(bwd)
+            res[name] = {"fwd_ms": fm, "bwd_ms": bm, "fwd_tflops": fl / fm / 1e9, "bwd_tflops": 2.5 * fl / bm / 1e9}
+        except Exception as e:  # backend not available for this shape / arch
+            res[name] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
+        box.pop("y", None)
+    return res
+
+
 def run_ours(args, world, rank, local_rank):
     import torch
     import torch.distributed as dist
@@ -268,12 +388,21 @@ def run_ours(args, world, rank, local_rank):
     blk = SkiparseBlock(g, heads, C, batch=1, group=group if world > 1 else None, log=log,
                         device=dev, ulysses_group=uly_group, transport=transport)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    x = torch.randn((blk.local_rows, blk.L_local, C), generator=gen, device=dev).to(torch.bfloat16)
-    gy = torch.randn((blk.local_rows, blk.L_local, C), generator=gen, device=dev).to(torch.bfloat16)
+    # one GPU: the step of SURVEY.md sec. 8d -- the unpadded original latent in, the block (orig ->
+    # TSA -> GSA -> orig) out; N GPUs: this rank's token-wise shard in and out (SSP steady state)
+    orig_step = world == 1 and blk._scatter is not None and not args.tsa_step
+    if orig_step:
+        shape = (1, T * H * W, C)
+        fn = blk.forward_original
+    else:
+        shape = (blk.local_rows, blk.L_local, C)
+        fn = blk
+    x = torch.randn(shape, generator=gen, device=dev).to(torch.bfloat16)
+    gy = torch.randn(shape, generator=gen, device=dev).to(torch.bfloat16)
     x.requires_grad_(True)
 
     def step(inp):
-        y = blk(inp)
+        y = fn(inp)
         y.backward(gy)
         return y
 
@@ -319,21 +448,28 @@ def run_ours(args, world, rank, local_rank):
     tokens_step = dp * T * H * W
     value = tokens_step / (ms_step / 1000.0)
 
-    # ---- end-to-end through the public API (pinned host input, loss read back).  Every step's
-    # input is copied host->device inside the timed region; the copy of step i+1 runs on a
-    # copy stream (double buffer) while step i computes, as a training loop's data feed would.
+    # ---- end-to-end through the public API: every step's input is copied host->device from
+    # pinned memory and its output y (the block's result, what the reference API returns) and the
+    # loss <y, gy> are copied back, all inside the timed region.  Copies run on two copy streams
+    # (double buffers) so step i+1's input upload and step i's output download overlap compute, as
+    # a training / serving loop's data feed would.
     host_x = torch.empty(tuple(x.shape), dtype=torch.bfloat16, pin_memory=True)
     host_x.copy_(x.detach().cpu())
+    host_y = [torch.empty(tuple(x.shape), dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
     host_loss = torch.empty((args.steps,), dtype=torch.float32, pin_memory=True)
     bufs = [torch.empty_like(x.detach()) for _ in range(2)]
     ready = [torch.cuda.Event() for _ in range(2)]
     consumed = [torch.cuda.Event() for _ in range(2)]
+    y_done = [torch.cuda.Event() for _ in range(2)]
     copy_stream = torch.cuda.Stream(device=dev)
+    d2h_stream = torch.cuda.Stream(device=dev)
+    ys = [None, None]
     barrier()
     torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     copy_stream.wait_stream(stream)
+    d2h_stream.wait_stream(stream)
     with torch.cuda.stream(copy_stream):
         bufs[0].copy_(host_x, non_blocking=True)
         ready[0].record(copy_stream)
@@ -348,12 +484,19 @@ def run_ours(args, world, rank, local_rank):
                 ready[nb].record(copy_stream)
         stream.wait_event(ready[b])
         xin = bufs[b].detach().requires_grad_(True)
-        y = blk(xin)
-        # the step's scalar loss <y, gy> as one dot-product pass (fp32 accumulate), read back below
+        y = fn(xin)
+        ys[b] = y.detach()
+        ys[b].record_stream(d2h_stream)       # y's memory is not reused before its download ends
+        y_done[b].record(stream)
+        with torch.cuda.stream(d2h_stream):
+            d2h_stream.wait_event(y_done[b])
+            host_y[b].copy_(ys[b], non_blocking=True)
+        # the step's scalar loss <y, gy> as one dot-product pass (fp32 accumulate)
         loss = torch.dot(y.detach().reshape(-1), gy.reshape(-1)).float()
         y.backward(gy)
         consumed[b].record(stream)
         host_loss[i:i + 1].copy_(loss.detach().view(1), non_blocking=True)
+    stream.wait_stream(d2h_stream)
     f1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -362,6 +505,7 @@ def run_ours(args, world, rank, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms_step = t.item() / args.steps
     e2e_value = tokens_step / (e2e_ms_step / 1000.0)
+    io_bytes = host_x.numel() * host_x.element_size()
 
     if rank != 0:
         return
@@ -400,7 +544,28 @@ def run_ours(args, world, rank, local_rank):
     roof["traffic_source"] = tsrc
     ftraffic, _ = _ncu_traffic("attn_fwd") if (args.config == "cfg3" and world == 1) else (None, None)
     roof["fwd_kernel"]["traffic"] = ftraffic
+    k1 = kern.get("gather_rows")
+    if k1 and orig_step:
+        # K1 row moves of the orig step: the unpadded latent -> compact TSA rows (forward) and its
+        # adjoint (backward); bytes = rows read + rows written, one C-wide bf16 row each
+        tin = blk._orig_plans()[0]
+        row_b = C * 2
+        by = [((tin.src >= 0).sum().item() + tin.src.numel()) * row_b,
+              ((tin.inv >= 0).sum().item() + tin.inv.numel()) * row_b]
+        alg = sum(by) / 2
+        k1t, k1src = _ncu_traffic("permute_rows_cfg3") if (args.config == "cfg3") else (None, None)
+        roof["k1"] = {"kernel": "osp_gather_rows (K1 permute_rows_warp)", "bound": "hbm",
+                      "achieved": alg / (k1["mean_ms"] / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                      "frac": alg / (k1["mean_ms"] / 1e3) / 1e9 / hbm,
+                      "algorithmic_bytes_per_launch": alg, "launches_per_step": k1["launches"] / args.steps,
+                      "traffic": k1t, "traffic_source": k1src}
     share = {n: v["total_ms"] / ms for n, v in kern.items()}
+    step_desc = ("orig -> TSA app -> GSA app -> orig (SURVEY.md sec. 8d): one K1 gather of the unpadded "
+                 "latent into compact TSA rows; application 1's epilogue stores into compact GSA rows, "
+                 "application 2's into the unpadded latent; backward mirrors it (K3 Delta pre-pass "
+                 "gathers dO, one K1 move returns dx); each application = fixed QKV projection (cuBLAS) "
+                 "+ tcgen05 attention; bwd = input grad") if orig_step else \
+        "TSA shard in -> TSA app + switch + GSA app + switch -> TSA shard out; bwd = input grad"
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong" if dp == 1 else "mixed",
@@ -411,19 +576,24 @@ def run_ours(args, world, rank, local_rank):
                                        + (f"xdp{dp}" if dp > 1 else "")),
                        "padded_grid": [blk.grid.t, blk.grid.h, blk.grid.w], "subseq_len": blk.L,
                        "l2": "inputs > 126 MB L2 (no flush needed)",
-                       "block": "TSA app + switch + GSA app + switch, each app = fixed QKV "
-                                "projection (cuBLAS) + tcgen05 attention; bwd = input grad"},
+                       "block": step_desc},
             "e2e": {"value": e2e_value, "unit": "tokens/s",
-                    "h2d_bytes_per_step": host_x.numel() * host_x.element_size(),
-                    "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms_step},
+                    "h2d_bytes_per_step": io_bytes,
+                    "d2h_bytes_per_step": io_bytes + 4, "ms_per_step": e2e_ms_step,
+                    "what": "x uploaded from pinned host memory, y and the loss downloaded, every step"},
             "gpu_launches": launches,
             "roofline": roof,
             "flops_per_step_per_gpu": fl,
             "kernel_ms": kern, "kernel_share_of_step": share,
             "comm": comm,
             "clocks": clk.summary()}
+    par = _parity_summary(args.config)
+    if par:
+        line["parity"] = par
+    if world == 1 and not args.no_comparator:
+        line["comparator"] = sdpa_comparator(heads, d, blk.L, blk.local_rows, dev)
     if world == 1 and not args.no_cpu:
-        cb = cpu_oracle_rate(args.config, 1, args.cpu_sample, reps=2)
+        cb = cpu_oracle_rate(args.config, 1, (args.cpu_sample, 2 * args.cpu_sample, 4 * args.cpu_sample))
         line["cpu_baseline"] = {k_: cb[k_] for k_ in ("value", "unit", "cores", "sample")}
         line["cpu_baseline"]["kind"] = "port"
     print(json.dumps(line), flush=True)
@@ -436,8 +606,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=2048)
+    ap.add_argument("--cpu-sample", type=int, default=2048,
+                    help="shortest CPU-oracle slice length (the fit also times 2x and 4x it)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-comparator", action="store_true", help="skip the same-box SDPA timings")
+    ap.add_argument("--tsa-step", action="store_true",
+                    help="N=1: time the token-wise steady-state block instead of the orig->orig step")
     ap.add_argument("--transport", default="auto", choices=["auto", "native", "hif8", "p2p"],
                     help="SSP switch transport for N > 1 (auto = native NCCL; p2p = K7 peer pull, one host)")
     args = ap.parse_args()

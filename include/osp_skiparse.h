@@ -157,6 +157,36 @@ int osp_attn_bwd_gather(const void* q, const void* k, const void* v, const void*
                         float scale, void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * K2/K3 with the Skiparse Rearrange fused into the output side (scatter mode), the production
+ * single-GPU block path.  q, k, v are contiguous per-sequence tiles as in osp_attn_fwd (each
+ * operand tile is re-read by many CTAs, so the loads stay plain TMA tiles), but output row j of
+ * sequence s is STORED to row out_index[s*capacity + j] of `out` (n_out_rows x >= heads*head_dim,
+ * row stride out_stride; -1 = not stored): the attention epilogue itself performs the pattern
+ * switch / padding expansion that follows attention (reference attention.py:131 and the block's
+ * tsa_to_gsa / gsa_to_tsa, skiparse.py:117-140), so no permuted copy is written by a separate
+ * pass.  zero_rows lists the n_zero_rows rows of `out` no sequence row lands on (pad tokens of
+ * the destination layout); the forward zero-fills them.  lse is (n_seq, heads, capacity).
+ * The backward reads O and dO through the same table: its Delta pre-pass (which reads both rows
+ * anyway) gathers dO into a contiguous operand image inside the workspace
+ * (>= osp_attn_bwd_scatter_workspace_bytes), and dq, dk, dv are written contiguously.
+ * Replaces: attention.py:119-131 (gather -> dense_attention -> zero pads -> inverse gather).
+ */
+int osp_attn_fwd_scatter(const void* q, const void* k, const void* v, void* out, float* lse,
+                         int64_t n_seq, int64_t capacity, int64_t heads, int64_t head_dim,
+                         int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t out_stride,
+                         const int32_t* seq_lens, const int32_t* out_index, int64_t n_out_rows,
+                         const int32_t* zero_rows, int64_t n_zero_rows, float scale, void* stream);
+size_t osp_attn_bwd_scatter_workspace_bytes(int64_t n_seq, int64_t capacity, int64_t heads,
+                                            int64_t head_dim);
+int osp_attn_bwd_scatter(const void* q, const void* k, const void* v, const void* out,
+                         const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                         int64_t n_seq, int64_t capacity, int64_t heads, int64_t head_dim,
+                         int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t out_stride,
+                         int64_t do_stride, int64_t dq_stride, int64_t dk_stride, int64_t dv_stride,
+                         const int32_t* seq_lens, const int32_t* out_index, int64_t n_out_rows,
+                         float scale, void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * K4: Sparse Sequence Parallel pattern switch, local steps of ssp_pattern_switch
  * (ssp.py:139-180; Alg. 1).  One rank's shard is (local_batch, L, chan) with
  * L = t*h*w/k^2, local_batch = G*b, G = k^2/group_size; (t,h,w,k) the padded global grid.

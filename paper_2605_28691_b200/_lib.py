@@ -44,6 +44,12 @@ _SIGS = {
     "osp_attn_bwd_gather": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp,
                              c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
                              c_i64, c_i64, c_f, c_vp, ctypes.c_size_t, c_vp], c_int),
+    "osp_attn_fwd_scatter": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
+                              c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_f, c_vp], c_int),
+    "osp_attn_bwd_scatter_workspace_bytes": ([c_i64, c_i64, c_i64, c_i64], ctypes.c_size_t),
+    "osp_attn_bwd_scatter": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64,
+                              c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp, c_vp,
+                              c_i64, c_f, c_vp, ctypes.c_size_t, c_vp], c_int),
     "osp_ssp_pack": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp],
                      c_int),
     "osp_ssp_unpack": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_vp],

@@ -26,7 +26,8 @@ from .gridseq import GridShape, SequenceTensor, default_device
 from .skiparse import SparsePattern, assignment_of, inverse_pattern_map, pattern_map
 
 __all__ = ["PROJECTION_SEED", "qkv_projections", "packed_projection", "project_qkv",
-           "dense_attention", "skiparse_attention", "attention_packed", "masked_dense_attention",
+           "dense_attention", "skiparse_attention", "attention_packed", "attention_scatter",
+           "masked_dense_attention",
            "pattern_allow_matrix", "skiparse_reference", "FlopReport",
            "flop_report"]
 
@@ -134,6 +135,46 @@ class _AttnGather(torch.autograd.Function):
                                 heads, d, plan.row_index, plan.lens, scale, dq=dqkv[:, :C],
                                 dk=dqkv[:, C:2 * C], dv=dqkv[:, 2 * C:])
         return dqkv, None, None, None, None
+
+
+class _AttnScatter(torch.autograd.Function):
+    """Attention over a packed (n_seq, cap, 3*C) [q | k | v] whose output rows are STORED through
+    a row table (compact.ScatterPlan): the rearrange / padding expansion that follows attention
+    runs in the K2 epilogue, and the backward's Delta pre-pass gathers dO through the same table."""
+
+    @staticmethod
+    def forward(ctx, qkv, heads, d, lens, plan, scale):
+        C = heads * d
+        q, k, v = qkv[..., :C], qkv[..., C:2 * C], qkv[..., 2 * C:]
+        out = torch.empty((plan.n_out_rows, C), dtype=qkv.dtype, device=qkv.device)
+        lse = kernels.attn_fwd_scatter(q, k, v, heads, d, lens, plan.out_index, out, plan.zero_rows, scale)
+        ctx.save_for_backward(qkv, out, lse)
+        ctx.cfg = (heads, d, lens, plan, scale)
+        return out.view(plan.out_shape)
+
+    @staticmethod
+    def backward(ctx, dout):
+        qkv, out, lse = ctx.saved_tensors
+        heads, d, lens, plan, scale = ctx.cfg
+        C = heads * d
+        dqkv = torch.empty_like(qkv)
+        kernels.attn_bwd_scatter(qkv[..., :C], qkv[..., C:2 * C], qkv[..., 2 * C:], out,
+                                 dout.reshape(-1, C), lse, heads, d, lens, plan.out_index, scale,
+                                 dqkv[..., :C], dqkv[..., C:2 * C], dqkv[..., 2 * C:])
+        return dqkv, None, None, None, None, None
+
+
+def attention_scatter(qkv: torch.Tensor, heads: int, lens: torch.Tensor, plan,
+                      scale: float | None = None) -> torch.Tensor:
+    """Per-subsequence attention over packed bf16 [q | k | v] (n_seq, cap, 3*C) whose output is
+    written straight into the next layout through plan (compact.ScatterPlan): returns a tensor of
+    plan.out_shape.  head_dim 64 or 128."""
+    C = qkv.shape[-1] // 3
+    d = C // heads
+    if heads * d != C or d not in (64, 128):
+        raise UnsupportedError("scatter-mode attention runs head_dim 64 or 128")
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    return _AttnScatter.apply(qkv.contiguous(), heads, d, lens, plan, scale)
 
 
 def attention_gather(qkv: torch.Tensor, heads: int, plan, scale: float | None = None) -> torch.Tensor:

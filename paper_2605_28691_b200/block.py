@@ -122,17 +122,39 @@ class SkiparseBlock:
         self.plan_gsa = self.pg.compact_plan(SparsePattern.GROUP_WISE, batch, (r0, r1)) if compact else None
         self._t2g = IndexMap._pattern("tsa_to_gsa", self.grid, batch)
         self._g2t = IndexMap._pattern("gsa_to_tsa", self.grid, batch)
-        # one GPU, head_dim 128: the rearranges are fused into the attention kernels' TMA loads and
-        # stores (gather mode) -- activations stay in the original latent layout end to end
+        # one GPU, head_dim 128: the rearranges can also be fused into the attention kernels' TMA
+        # LOADS (gather mode, forward_original_gather) -- exact but slower
         self.gather = None
         if self.world == 1 and chan // heads == 128:
             from .compact import gather_plan
             self.gather = (gather_plan(g, SparsePattern.TOKEN_WISE, batch, self.pg, "original"),
                            gather_plan(g, SparsePattern.GROUP_WISE, batch, self.pg, "original"))
-        # one GPU with compaction: fold expand -> pattern switch -> compact into one row move
-        # each way (compact TSA -> compact GSA, compact GSA -> padded TSA)
+        # one GPU (the benched path): every rearrange that follows an attention application runs
+        # in its epilogue (scatter mode): application 1 stores its compact TSA rows straight into
+        # the compact GSA layout application 2 projects, application 2 stores into the block's
+        # output layout; the backward's Delta pre-pass gathers dO through the same tables.  On an
+        # unpadded grid the "compact" plans are the identity plans (every row real).
+        self._scatter = None
         self._fused = None
-        if self.world == 1 and self.plan_tsa is not None and not (qk_norm is not None or rope):
+        self._orig = None
+        d = chan // heads
+        if self.world == 1 and compact and not self.prologue and d in (64, 128):
+            from .compact import compact_plan, scatter_plan
+            if self.plan_tsa is None:   # trivial grid: identity plans
+                full = compact_plan(torch.ones(self.local_rows, self.L, dtype=torch.bool, device=dev))
+                self.plan_tsa = self.plan_gsa = full
+            pt, pgs = self.plan_tsa, self.plan_gsa
+            t2g = self._t2g.src.reshape(-1).to(dev)          # padded GSA row x holds TSA row t2g[x]
+            g2t = self._g2t.src.reshape(-1).to(dev)          # padded TSA row y holds GSA row g2t[y]
+            pgt = pt.gather                                   # compact TSA row -> padded TSA row
+            a = torch.where(pgt >= 0, pgs.scatter[g2t[pgt.clamp(min=0)]], torch.full_like(pgt, -1))
+            pgg = pgs.gather                                  # compact GSA row -> padded GSA row
+            b = torch.where(pgg >= 0, t2g[pgg.clamp(min=0)], torch.full_like(pgg, -1))
+            self._scatter = (
+                scatter_plan(a, pt.n_seq, pt.cap, pgs.n_seq * pgs.cap, (pgs.n_seq, pgs.cap, chan)),
+                scatter_plan(b, pgs.n_seq, pgs.cap, self.local_rows * self.L, (self.local_rows, self.L, chan)))
+        elif self.world == 1 and self.plan_tsa is not None and not self.prologue:
+            # other head dims: fold expand -> pattern switch -> compact into one K1 row move each way
             from .compact import row_move
             pt, pgs = self.plan_tsa, self.plan_gsa
             t2g = self._t2g.src.reshape(-1)                 # padded GSA row <- padded TSA row
@@ -237,11 +259,52 @@ class SkiparseBlock:
             return expand_rows(o, plan) if expand else o
         return attention_packed(qkv, self.heads, bits, zero_invalid_queries=bits is not None)
 
+    def _orig_plans(self):
+        """Tables of the original-layout step (orig -> TSA -> GSA -> orig): the
+        K1 gather of the unpadded latent into compact TSA rows, and application 2's scatter
+        straight into the unpadded latent (every real token is one compact GSA row)."""
+        if self._orig is None:
+            from .compact import row_move, scatter_plan
+            dev = self.W1.device
+            p, B = self.grid, self.batch
+            S = p.seq_len
+            mask = self.pg.mask.to(dev).bool() if not self.pg.trivial else torch.ones(S, dtype=torch.bool, device=dev)
+            real_idx = torch.cumsum(mask.to(torch.int64), 0) - 1
+            S_real = int(mask.sum())
+
+            def real_row(src):        # padded (batch, token) flat index -> unpadded latent row
+                return (src // S) * S_real + real_idx[src % S]
+
+            o2t = IndexMap._pattern("orig_to_tsa", p, B).src.reshape(-1).to(dev)
+            o2g = IndexMap._pattern("orig_to_gsa", p, B).src.reshape(-1).to(dev)
+            pt, pgs = self.plan_tsa, self.plan_gsa
+            tin = torch.where(pt.gather >= 0, real_row(o2t[pt.gather.clamp(min=0)]), torch.full_like(pt.gather, -1))
+            bo = torch.where(pgs.gather >= 0, real_row(o2g[pgs.gather.clamp(min=0)]), torch.full_like(pgs.gather, -1))
+            self._orig = (row_move(tin, B * S_real, pt.cap, S_real),
+                          scatter_plan(bo, pgs.n_seq, pgs.cap, B * S_real, (B, S_real, self.chan)))
+        return self._orig
+
     def forward_original(self, x: torch.Tensor) -> torch.Tensor:
+        """One GPU: the block on the original (unpadded) latent layout (B, T*H0*W0, C) ->
+        same layout.  One K1 row gather brings the latent into compact TSA rows for the first
+        projection GEMM; every later rearrange runs in an attention epilogue (application 1 ->
+        compact GSA rows, application 2 -> the unpadded latent), and their backward adjoints in
+        the attention backward's Delta pre-pass."""
+        if self._scatter is None:
+            raise ValueError("forward_original needs one GPU, head_dim 64/128 and no projection prologue")
+        from .attention import attention_scatter
+        from .compact import apply_move
+        tin, bo = self._orig_plans()
+        pt, pgs = self.plan_tsa, self.plan_gsa
+        x1 = apply_move(x.reshape(-1, self.chan), tin)
+        x2 = attention_scatter(torch.matmul(x1, self.W1), self.heads, pt.lens, self._scatter[0])
+        return attention_scatter(torch.matmul(x2, self.W2), self.heads, pgs.lens, bo)
+
+    def forward_original_gather(self, x: torch.Tensor) -> torch.Tensor:
         """One GPU: the block on the original (unpadded) latent layout (B, T*H0*W0, C) -- TSA
         application then GSA application with no rearranged copy in HBM (gather-mode kernels)."""
         if self.gather is None:
-            raise ValueError("forward_original needs one GPU and head_dim 128")
+            raise ValueError("forward_original_gather needs one GPU and head_dim 128")
         from .attention import attention_gather
         for W, Wt, plan, pat in ((self.W1, getattr(self, "W1t", None), self.gather[0], SparsePattern.TOKEN_WISE),
                                  (self.W2, getattr(self, "W2t", None), self.gather[1], SparsePattern.GROUP_WISE)):
@@ -253,6 +316,14 @@ class SkiparseBlock:
                 qkv = torch.matmul(x, W)
             x = attention_gather(qkv, self.heads, plan)
         return x
+
+    def _call_scatter(self, x_tsa):
+        from .attention import attention_scatter
+        from .compact import compact_rows
+        pt, pgs = self.plan_tsa, self.plan_gsa
+        a, b = self._scatter
+        x2 = attention_scatter(torch.matmul(compact_rows(x_tsa, pt), self.W1), self.heads, pt.lens, a)
+        return attention_scatter(torch.matmul(x2, self.W2), self.heads, pgs.lens, b)
 
     def _call_fused(self, x_tsa):
         from .compact import apply_move, compact_rows
@@ -273,6 +344,8 @@ class SkiparseBlock:
 
     def __call__(self, x_tsa: torch.Tensor) -> torch.Tensor:
         """x_tsa: this rank's (G*B, L, C) bf16 shard in the token-wise layout."""
+        if self._scatter is not None:
+            return self._call_scatter(x_tsa)
         if self._fused is not None:
             return self._call_fused(x_tsa)
         if self._peer is not None:

@@ -19,7 +19,7 @@ import torch
 from . import kernels
 
 __all__ = ["CompactPlan", "compact_plan", "compact_rows", "expand_rows", "RowMove", "row_move",
-           "GatherPlan", "gather_plan"]
+           "GatherPlan", "gather_plan", "ScatterPlan", "scatter_plan"]
 
 
 @dataclass(frozen=True)
@@ -125,6 +125,33 @@ class _Move(torch.autograd.Function):
 
 def apply_move(x: torch.Tensor, mv: RowMove) -> torch.Tensor:
     return _Move.apply(x, mv)
+
+
+@dataclass(frozen=True)
+class ScatterPlan:
+    """Output-side row table of the scatter-mode attention (K2 epilogue / K3 Delta pre-pass):
+    row j of compact sequence s is stored to destination row out_index[s, j] (-1 = dropped);
+    zero_rows are the destination rows no source lands on (zero-filled by the forward)."""
+
+    out_index: torch.Tensor            # (n_seq, cap) int32
+    zero_rows: torch.Tensor | None     # (n_zero,) int32
+    n_out_rows: int
+    out_shape: tuple                   # view of the (n_out_rows, C) output
+
+
+def scatter_plan(out_index: torch.Tensor, n_seq: int, cap: int, n_out_rows: int,
+                 out_shape: tuple) -> ScatterPlan:
+    """out_index (n_seq*cap,) int64: destination row of every source row (-1 = none); the map
+    must be injective."""
+    oi = out_index.to(torch.int64).reshape(-1)
+    hit = torch.zeros(n_out_rows, dtype=torch.bool, device=oi.device)
+    ok = oi >= 0
+    hit[oi[ok]] = True
+    if int(hit.sum()) != int(ok.sum()):
+        raise ValueError("scatter plan is not injective")
+    zero = torch.nonzero(~hit).view(-1).to(torch.int32).contiguous()
+    return ScatterPlan(oi.view(n_seq, cap).to(torch.int32).contiguous(), zero if zero.numel() else None,
+                       n_out_rows, tuple(out_shape))
 
 
 @dataclass(frozen=True)

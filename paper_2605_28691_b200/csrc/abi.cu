@@ -382,6 +382,72 @@ int osp_attn_bwd_gather(const void* q, const void* k, const void* v, const void*
                          workspace, workspace_bytes, as_stream(stream));
 }
 
+static int scatter_checks(const int32_t* seq_lens, const int32_t* out_index, int64_t n_out_rows,
+                          int64_t out_stride, const void* out) {
+  if (!seq_lens || !out_index || n_out_rows <= 0 || n_out_rows >= (int64_t(1) << 31)) {
+    set_error("scatter attention needs seq_lens, out_index and 0 < n_out_rows < 2^31");
+    return kValue;
+  }
+  if ((out_stride * 2) % 16 || (reinterpret_cast<uintptr_t>(out) & 15)) {
+    set_error("output needs 16-byte aligned base and row stride");
+    return kValue;
+  }
+  return kOk;
+}
+
+int osp_attn_fwd_scatter(const void* q, const void* k, const void* v, void* out, float* lse,
+                         int64_t n_seq, int64_t capacity, int64_t heads, int64_t head_dim,
+                         int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t out_stride,
+                         const int32_t* seq_lens, const int32_t* out_index, int64_t n_out_rows,
+                         const int32_t* zero_rows, int64_t n_zero_rows, float scale, void* stream) {
+  int rc = attn_checks(n_seq, capacity, heads, head_dim);
+  if (rc != kOk) return rc;
+  if ((rc = scatter_checks(seq_lens, out_index, n_out_rows, out_stride, out)) != kOk) return rc;
+  if (n_zero_rows < 0 || n_zero_rows > n_out_rows || (n_zero_rows && !zero_rows)) {
+    set_error("zero_rows must list 0 <= n_zero_rows <= n_out_rows rows");
+    return kValue;
+  }
+  AttnShape s{n_seq, capacity, heads, head_dim, seq_lens};
+  s.out_index = out_index;
+  s.zero_rows = zero_rows;
+  s.n_zero = n_zero_rows;
+  return launch_attn_fwd(q, k, v, out, lse, s, q_stride, k_stride, v_stride, out_stride, nullptr, 0,
+                         scale, as_stream(stream));
+}
+
+size_t osp_attn_bwd_scatter_workspace_bytes(int64_t n_seq, int64_t capacity, int64_t heads,
+                                            int64_t head_dim) {
+  AttnShape s{n_seq, capacity, heads, head_dim};
+  return attn_bwd_workspace_bytes(s) + static_cast<size_t>(n_seq * capacity * heads * head_dim * 2);
+}
+
+int osp_attn_bwd_scatter(const void* q, const void* k, const void* v, const void* out,
+                         const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                         int64_t n_seq, int64_t capacity, int64_t heads, int64_t head_dim,
+                         int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t out_stride,
+                         int64_t do_stride, int64_t dq_stride, int64_t dk_stride, int64_t dv_stride,
+                         const int32_t* seq_lens, const int32_t* out_index, int64_t n_out_rows,
+                         float scale, void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = attn_checks(n_seq, capacity, heads, head_dim);
+  if (rc != kOk) return rc;
+  if ((rc = scatter_checks(seq_lens, out_index, n_out_rows, out_stride, out)) != kOk) return rc;
+  if ((do_stride * 2) % 16 || (reinterpret_cast<uintptr_t>(dout) & 15)) {
+    set_error("dout needs 16-byte aligned base and row stride");
+    return kValue;
+  }
+  AttnShape s{n_seq, capacity, heads, head_dim, seq_lens};
+  const size_t base = attn_bwd_workspace_bytes(s);
+  if (workspace_bytes < osp_attn_bwd_scatter_workspace_bytes(n_seq, capacity, heads, head_dim)) {
+    set_error("attention backward workspace too small (osp_attn_bwd_scatter_workspace_bytes)");
+    return kValue;
+  }
+  s.out_index = out_index;
+  s.do_image = static_cast<uint8_t*>(workspace) + base;
+  return launch_attn_bwd(q, k, v, out, dout, lse, dq, dk, dv, s, q_stride, k_stride, v_stride,
+                         out_stride, do_stride, dq_stride, dk_stride, dv_stride, nullptr, 0, scale,
+                         workspace, workspace_bytes, as_stream(stream));
+}
+
 static int ssp_params(MapParams& p, int kind, int64_t group_size, int64_t local_batch, int64_t t,
                       int64_t h, int64_t w, int64_t k) {
   int rc = grid_error(t, h, w, k);

@@ -942,12 +942,16 @@ __global__ void dq_finalize_v2_kernel(const float* __restrict__ acc, __nv_bfloat
 
 // delta and log2-domain lse per (seq, head, query), padded to seq_pad.  D/8 lanes per row, each
 // with one 16-byte load of O and of dO (a row's head slice is one contiguous 2*D-byte segment).
+// Scatter mode (out_index): O and dO rows are read through the forward's output table and the
+// dO head slice is also written to the contiguous operand image do_image (n_seq, seq_len, heads*D),
+// zeros past the sequence length -- the gather of dO rides on this pass, which reads them anyway.
 template <int D>
 __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t o_stride,
                                 const __nv_bfloat16* __restrict__ dout, int64_t do_stride,
                                 const float* __restrict__ lse, float* lse2, float* delta, int64_t n_seq,
                                 int heads, int seq_len, int seq_pad, const int* __restrict__ seq_lens,
-                                const int* __restrict__ row_index) {
+                                const int* __restrict__ row_index, const int* __restrict__ out_index,
+                                __nv_bfloat16* __restrict__ do_image) {
   constexpr int G = D / 8;             // lanes per row
   constexpr int R = 32 / G;            // rows per warp
   const int64_t total = n_seq * heads * static_cast<int64_t>(seq_pad);
@@ -955,6 +959,7 @@ __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t o_s
   const int sub = lane / G, gl = lane % G;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int* tab = row_index ? row_index : out_index;
   for (int64_t wb = warp0 * R; wb < total; wb += nwarps * R) {
     const int64_t w = wb + sub;
     const bool in = w < total;
@@ -968,19 +973,25 @@ __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, int64_t o_s
     const int64_t s = sh32 / static_cast<uint32_t>(heads);
     const int len = seq_lens ? __ldg(seq_lens + s) : seq_len;
     float acc = 0.f;
+    uint4 dv = make_uint4(0u, 0u, 0u, 0u);
     if (in && q < len) {
-      const int64_t row = row_index ? row_index[s * seq_len + q] : s * seq_len + q;
-      const uint4 ov = *reinterpret_cast<const uint4*>(o + row * o_stride + static_cast<int64_t>(h) * D + gl * 8);
-      const uint4 dv = *reinterpret_cast<const uint4*>(dout + row * do_stride + static_cast<int64_t>(h) * D + gl * 8);
-      const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
-      const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+      const int64_t row = tab ? __ldg(tab + s * seq_len + q) : s * seq_len + q;
+      if (row >= 0) {
+        const uint4 ov = *reinterpret_cast<const uint4*>(o + row * o_stride + static_cast<int64_t>(h) * D + gl * 8);
+        dv = *reinterpret_cast<const uint4*>(dout + row * do_stride + static_cast<int64_t>(h) * D + gl * 8);
+        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+        const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float2 of = __bfloat1622float2(o2[j]);
-        const float2 df = __bfloat1622float2(d2[j]);
-        acc += of.x * df.x + of.y * df.y;
+        for (int j = 0; j < 4; ++j) {
+          const float2 of = __bfloat1622float2(o2[j]);
+          const float2 df = __bfloat1622float2(d2[j]);
+          acc += of.x * df.x + of.y * df.y;
+        }
       }
     }
+    if (do_image && in && q < seq_len)
+      *reinterpret_cast<uint4*>(do_image + (s * seq_len + q) * (static_cast<int64_t>(heads) * D) +
+                                static_cast<int64_t>(h) * D + gl * 8) = dv;
 #pragma unroll
     for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, off);
     if (in && gl == 0) {
@@ -1054,9 +1065,14 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     bwd_prep_kernel<D><<<grid_for(rows * 32 / (32 / (D / 8)), 256), 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(o), os, static_cast<const __nv_bfloat16*>(dout), dos, lse,
         w.lse2, w.delta, s.n_seq, static_cast<int>(s.heads), static_cast<int>(s.seq_len),
-        static_cast<int>(seq_pad), s.seq_lens, s.row_index);
+        static_cast<int>(seq_pad), s.seq_lens, s.row_index, s.out_index,
+        static_cast<__nv_bfloat16*>(s.out_index ? s.do_image : nullptr));
     rc = check_cuda(cudaGetLastError(), "bwd_prep launch");
     if (rc != kOk) return rc;
+  }
+  if (s.out_index) {  // scatter mode: the main kernel reads the contiguous dO image
+    dout = s.do_image;
+    dos = s.heads * D;
   }
   CUtensorMap mq, mk, mv, mdo;
   const int64_t cols = s.heads * D;

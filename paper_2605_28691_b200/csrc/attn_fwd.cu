@@ -51,6 +51,9 @@ struct FwdArgs {
   const int* seq_lens;      // per-sequence valid length (<= seq_len) or null
   const int* row_index;     // gather mode: (n_seq, seq_len) token rows of q/k/v/o (-1 = none)
   int n_rows;               // gather mode: rows of the q/k/v/o tensors
+  const int* out_index;     // scatter mode: (n_seq, seq_len) destination rows of o (-1 = none)
+  const int* zero_rows;     // scatter mode: destination rows with no source (zero-filled)
+  int n_zero;
   int heads;
   float scale_log2;
   int zero_invalid_q;
@@ -96,9 +99,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int q_row0 = blockIdx.x * 2 * kBM;
   // variable-length sequences: rows >= len are neither keys nor queries (compacted layouts)
   const int len = a.seq_lens ? __ldg(a.seq_lens + seq) : a.seq_len;
+  if (a.n_zero && warp == 3) {
+    // scatter mode: this CTA's share of the destination rows no sequence row lands on (disjoint
+    // from every stored row), head slice `head`; 16 lanes x 16 B per 128-d row
+    const int64_t n_cta = static_cast<int64_t>(gridDim.x) * gridDim.z;
+    const int64_t b = blockIdx.x + static_cast<int64_t>(gridDim.x) * blockIdx.z;
+    const int64_t r0 = b * a.n_zero / n_cta, r1 = (b + 1) * a.n_zero / n_cta;
+    constexpr int kLanesPerRow = D / 8;
+    constexpr int kRowsPerIter = 32 / kLanesPerRow;
+    for (int64_t r = r0 + lane / kLanesPerRow; r < r1; r += kRowsPerIter) {
+      const int64_t row = __ldg(a.zero_rows + r);
+      *reinterpret_cast<uint4*>(a.o + row * a.o_stride + static_cast<int64_t>(head) * D +
+                                (lane % kLanesPerRow) * 8) = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
   if (q_row0 >= len) {  // whole CTA past the sequence: o rows 0, lse +inf
     const int r1 = min(q_row0 + 2 * kBM, a.seq_len);
-    if (!a.row_index)  // gather mode: rows past the length have no destination
+    if (!a.row_index && !a.out_index)  // gather / scatter mode: rows past the length have no destination
       zero_rows_bf16(a.o + static_cast<int64_t>(seq) * a.seq_len * a.o_stride + static_cast<int64_t>(head) * D,
                      a.o_stride, q_row0, r1, D);
     for (int r = q_row0 + static_cast<int>(threadIdx.x); r < r1; r += blockDim.x)
@@ -420,10 +437,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (a.zero_invalid_q && vbits && row_ok) q_valid = bit_at(vbits, a.words_per_seq, q_row);
     const bool live = row_ok && q_valid && l > 0.f;
     const float inv_l = live ? 1.f / l : 0.f;
+    const int* tab = a.row_index ? a.row_index : a.out_index;
     const int64_t out_row =
-        a.row_index ? (row_ok ? a.row_index[static_cast<int64_t>(seq) * a.seq_len + q_row] : -1)
-                    : static_cast<int64_t>(seq) * a.seq_len + q_row;
-    const bool write_o = a.row_index ? out_row >= 0 : in_cap;
+        tab ? (row_ok ? __ldg(tab + static_cast<int64_t>(seq) * a.seq_len + q_row) : -1)
+            : static_cast<int64_t>(seq) * a.seq_len + q_row;
+    const bool write_o = tab ? out_row >= 0 : in_cap;
     __nv_bfloat16* orow = a.o + out_row * a.o_stride + static_cast<int64_t>(head) * D;
 #pragma unroll
     for (int cc = 0; cc < D / 32; ++cc) {
@@ -487,6 +505,9 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
   a.seq_lens = s.seq_lens;
   a.row_index = s.row_index;
   a.n_rows = static_cast<int>(s.n_rows);
+  a.out_index = s.out_index;
+  a.zero_rows = s.zero_rows;
+  a.n_zero = static_cast<int>(s.n_zero);
   a.scale_log2 = scale * 1.4426950408889634f;
   a.zero_invalid_q = zero_invalid_q;
   {

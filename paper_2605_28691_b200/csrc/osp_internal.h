@@ -64,6 +64,15 @@ struct AttnShape {
   // layout; row j of sequence s is row row_index[s * seq_len + j] (-1 = none)
   const int32_t* row_index = nullptr;
   int64_t n_rows = 0;
+  // scatter mode (operands contiguous, output through a row table): o row j of sequence s is row
+  // out_index[s * seq_len + j] of an (n_out_rows, >= heads*head_dim) tensor (-1 = not stored),
+  // zero_rows the rows of that tensor no sequence row lands on (zero-filled by the forward).  The
+  // backward reads O and dO through the same table; its prologue writes the contiguous dO operand
+  // image do_image (n_seq, seq_len, heads*head_dim) on the way.
+  const int32_t* out_index = nullptr;
+  const int32_t* zero_rows = nullptr;
+  int64_t n_zero = 0;
+  void* do_image = nullptr;
 };
 
 int launch_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,

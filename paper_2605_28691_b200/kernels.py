@@ -305,6 +305,56 @@ def attn_bwd_gather(q, k, v, o, do, lse, heads: int, head_dim: int, row_index, s
     return dq, dk, dv
 
 
+def attn_fwd_scatter(q, k, v, heads: int, head_dim: int, seq_lens: torch.Tensor, out_index: torch.Tensor,
+                     out: torch.Tensor, zero_rows: torch.Tensor | None, scale: float):
+    """Scatter-mode attention: q, k, v (n_seq, cap, >= C) contiguous per-sequence rows as in
+    attn_fwd; output row j of sequence s is stored to row out_index[s, j] of `out` (n_out_rows, C)
+    (-1 = not stored) and the rows listed in zero_rows are zero-filled.  Returns lse
+    (n_seq, heads, cap)."""
+    L = _lib.lib()
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        _cuda(t, name)
+        if t.dtype != torch.bfloat16:
+            raise UnsupportedError(f"{name} must be bfloat16, got {t.dtype}")
+        if t.stride(-1) != 1 or t.stride(0) != t.shape[1] * t.stride(1):
+            raise ShapeError(f"{name} needs unit column stride and dense rows")
+    n_seq, cap = q.shape[0], q.shape[1]
+    if tuple(out_index.shape) != (n_seq, cap) or out_index.dtype != torch.int32:
+        raise ShapeError(f"out_index must be ({n_seq}, {cap}) int32")
+    if out.dim() != 2 or out.stride(1) != 1:
+        raise ShapeError("out must be a (rows, C) tensor with unit column stride")
+    lse = torch.empty((n_seq, heads, cap), dtype=torch.float32, device=q.device)
+    lens = _lens(seq_lens, n_seq, cap)
+    nz = 0 if zero_rows is None else zero_rows.numel()
+    _lib.check(STATS.run('attn_fwd', 1, lambda: L.osp_attn_fwd_scatter(
+        q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr(), n_seq, cap, heads,
+        head_dim, q.stride(1), k.stride(1), v.stride(1), out.stride(0), lens.data_ptr(),
+        out_index.data_ptr(), out.shape[0], _lib.ptr(zero_rows) if nz else 0, nz, float(scale),
+        _lib.stream_ptr(q.device))))
+    return lse
+
+
+def attn_bwd_scatter(q, k, v, out, dout, lse, heads: int, head_dim: int, seq_lens, out_index,
+                     scale: float, dq, dk, dv):
+    """Backward of attn_fwd_scatter: out / dout are the scattered (n_out_rows, C) output and its
+    gradient (read through out_index); dq, dk, dv are contiguous (n_seq, cap, C) views."""
+    L = _lib.lib()
+    n_seq, cap = q.shape[0], q.shape[1]
+    dev = q.device
+    if dout.stride(-1) != 1:
+        dout = dout.contiguous()
+    ws_bytes = L.osp_attn_bwd_scatter_workspace_bytes(n_seq, cap, heads, head_dim)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    lens = _lens(seq_lens, n_seq, cap)
+    _lib.check(STATS.run('attn_bwd', 3, lambda: L.osp_attn_bwd_scatter(
+        q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+        dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), n_seq, cap, heads, head_dim, q.stride(1),
+        k.stride(1), v.stride(1), out.stride(0), dout.stride(0), dq.stride(1), dk.stride(1),
+        dv.stride(1), lens.data_ptr(), out_index.data_ptr(), out.shape[0], float(scale), ws.data_ptr(),
+        ws_bytes, _lib.stream_ptr(dev))))
+    return dq, dk, dv
+
+
 def ssp_pack(x: torch.Tensor, group_size: int, t: int, h: int, w: int, k: int) -> torch.Tensor:
     L = _lib.lib()
     _cuda(x, "x")

@@ -335,7 +335,7 @@ def test_block_compaction_paths_agree_fwd_bwd(P):
     C, heads = 256, 2
     a = SkiparseBlock(g, heads, C)
     b = SkiparseBlock(g, heads, C, compact=False)
-    assert a._fused is not None and b.plan_tsa is None
+    assert a._scatter is not None and b.plan_tsa is None
     torch.manual_seed(3)
     x = torch.randn(a.local_rows, a.L, C, device="cuda").to(torch.bfloat16)
     xa, xb = x.clone().requires_grad_(True), x.clone().requires_grad_(True)
@@ -351,10 +351,12 @@ def test_block_compaction_paths_agree_fwd_bwd(P):
     assert rel < 2e-2, rel
 
 
+@pytest.mark.parametrize("method", ["forward_original", "forward_original_gather"])
 @pytest.mark.parametrize("grid", [(2, 10, 12, 2), (2, 8, 16, 2)])
-def test_block_forward_original_matches_pattern_layout_block(P, grid):
-    """Gather-mode block (rearranges fused into the attention kernels, original unpadded layout)
-    equals the pattern-layout block composed with explicit rearranges, fwd and input grad."""
+def test_block_forward_original_matches_pattern_layout_block(P, grid, method):
+    """Original-layout block (scatter mode: rearranges in the attention epilogues; gather mode:
+    in the TMA loads) equals the pattern-layout block composed with explicit rearranges, fwd and
+    input grad."""
     from paper_2605_28691_b200.block import SkiparseBlock
     g = P.GridShape(*grid)
     pg = P.pad_grid(g)
@@ -364,7 +366,7 @@ def test_block_forward_original_matches_pattern_layout_block(P, grid):
     torch.manual_seed(4)
     x = torch.randn(1, g.seq_len, C, device="cuda").to(torch.bfloat16)
     xa = x.clone().requires_grad_(True)
-    ya = blk.forward_original(xa)
+    ya = getattr(blk, method)(xa)
     xt = blk.to_local_tsa(x).detach().requires_grad_(True)
     yt = blk(xt)
     p = pg.padded
@@ -384,7 +386,7 @@ def test_block_forward_original_with_prologue(P):
     g = P.GridShape(2, 10, 12, 2)
     blk = SkiparseBlock(g, 2, 256, qk_norm="head", rope=True)
     x = torch.randn(1, g.seq_len, 256, device="cuda").to(torch.bfloat16).requires_grad_(True)
-    y = blk.forward_original(x)
+    y = blk.forward_original_gather(x)
     y.float().sum().backward()
     assert torch.isfinite(y).all() and torch.isfinite(x.grad).all()
 

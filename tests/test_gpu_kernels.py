@@ -319,3 +319,51 @@ def test_attention_repeatable_bitwise(lib):
         assert torch.equal(cur[0], ref[0]) and torch.equal(cur[1], ref[1])
         assert torch.equal(cur[3], ref[3]) and torch.equal(cur[4], ref[4])
         assert torch.allclose(cur[2], ref[2], rtol=2 ** -6, atol=1e-6)   # bf16 ulp flips only
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("lens", [(300, 257, 1, 0), (512, 384, 200, 450)])
+def test_attention_scatter_mode_bitexact_vs_contiguous(lib, lens, d):
+    """Scatter mode (output rows stored through a row table, zero-filled uncovered rows; the
+    backward gathers O / dO through the same table) computes bit for bit what the contiguous
+    kernels compute followed by an explicit scatter / gather."""
+    from paper_2605_28691_b200 import kernels
+    torch.manual_seed(21)
+    heads = 2
+    C = heads * d
+    n, cap = len(lens), 512
+    scale = 1 / math.sqrt(d)
+    qkv = torch.randn(n, cap, 3 * C, device=_dev()).bfloat16()
+    q, k, v = qkv[..., :C], qkv[..., C:2 * C], qkv[..., 2 * C:]
+    sl = torch.tensor(lens, dtype=torch.int32, device=_dev())
+    o_ref, lse_ref = kernels.attn_fwd(q, k, v, heads, d, None, False, scale, seq_lens=sl)
+    # injective table: the real rows of every sequence land on a random permutation of n_out rows
+    n_out = sum(lens) + 97
+    perm = torch.randperm(n_out, device=_dev())
+    out_index = torch.full((n, cap), -1, dtype=torch.int64, device=_dev())
+    i = 0
+    for s, ln in enumerate(lens):
+        out_index[s, :ln] = perm[i:i + ln]
+        i += ln
+    from paper_2605_28691_b200.compact import scatter_plan
+    plan = scatter_plan(out_index.view(-1), n, cap, n_out, (n_out, C))
+    assert plan.zero_rows.numel() == 97
+    out = torch.full((n_out, C), float("nan"), device=_dev()).bfloat16()
+    lse = kernels.attn_fwd_scatter(q, k, v, heads, d, sl, plan.out_index, out, plan.zero_rows, scale)
+    want = torch.zeros(n_out, C, device=_dev()).bfloat16()
+    ok = out_index >= 0
+    want[out_index[ok]] = o_ref[ok]
+    assert torch.equal(out, want)
+    for s, ln in enumerate(lens):
+        assert torch.equal(lse[s, :, :ln], lse_ref[s, :, :ln])
+    # backward: dout lives in the scattered layout
+    dout = torch.randn(n_out, C, device=_dev()).bfloat16()
+    do_c = torch.zeros(n, cap, C, device=_dev()).bfloat16()
+    do_c[ok] = dout[out_index[ok]]
+    dq_r, dk_r, dv_r = kernels.attn_bwd(q, k, v, o_ref, do_c, lse_ref, heads, d, None, False, scale, seq_lens=sl)
+    dqkv = torch.empty_like(qkv)
+    kernels.attn_bwd_scatter(q, k, v, out, dout, lse, heads, d, sl, plan.out_index, scale,
+                             dqkv[..., :C], dqkv[..., C:2 * C], dqkv[..., 2 * C:])
+    for s, ln in enumerate(lens):
+        for got, r in zip((dqkv[..., :C], dqkv[..., C:2 * C], dqkv[..., 2 * C:]), (dq_r, dk_r, dv_r)):
+            assert torch.equal(got[s, :ln], r[s, :ln])
