@@ -82,6 +82,20 @@ int osp_rearrange(const void* src, void* dst, int64_t elem_bytes, int64_t chan, 
  * zero rows (the Python shim validates tables as gridseq.py:140-150 does). */
 int osp_gather_rows(const void* src, void* dst, const int64_t* index, int64_t n_out_rows,
                     int64_t n_in_rows, int64_t row_bytes, void* stream);
+
+/*
+ * Table gather over channel-chunked layouts (bytes strides): for every output row r and chunk
+ * c < n_chunks, chunk_bytes are copied from src + c*src_chunk_stride + index[r]*src_row_stride to
+ * dst + c*dst_chunk_stride + r*dst_row_stride (index[r] < 0 or >= n_in_rows: zeros).  The SSP
+ * switch's local step when its all-to-all runs per head chunk overlapped with attention
+ * (ssp.py:166-178 unpack, composed with the block's compaction; and the pack of a gradient into
+ * per-chunk send blocks); the channel-split identity (pkg/tests/test_ssp.py:167-178) makes the
+ * chunked switch equal the whole one.
+ */
+int osp_gather_rows_chunked(const void* src, void* dst, const int64_t* index, int64_t n_out_rows,
+                            int64_t n_in_rows, int64_t n_chunks, int64_t chunk_bytes,
+                            int64_t src_row_stride, int64_t src_chunk_stride, int64_t dst_row_stride,
+                            int64_t dst_chunk_stride, void* stream);
 /* IndexMap.invert (gridseq.py:179-185): inv[index[i]] = i. */
 int osp_invert_index(const int64_t* index, int64_t* inv, int64_t n, void* stream);
 

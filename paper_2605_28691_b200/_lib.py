@@ -28,6 +28,8 @@ _SIGS = {
     "osp_rearrange": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_i64,
                        c_i64, c_vp], c_int),
     "osp_gather_rows": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp], c_int),
+    "osp_gather_rows_chunked": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64,
+                                 c_vp], c_int),
     "osp_invert_index": ([c_vp, c_vp, c_i64, c_vp], c_int),
     "osp_pattern_mask_bits": ([c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_i64, c_i64, c_vp],
                               c_int),

@@ -66,7 +66,7 @@ class SkiparseBlock:
     def __init__(self, g: GridShape, heads: int, chan: int, batch: int = 1, group=None,
                  log: CommLog | None = None, device=None, seeds=(PROJECTION_SEED, PROJECTION_SEED + 1),
                  transport: str = "native", qk_norm: str | None = None, rope: bool = False,
-                 eps: float = 1e-6, compact: bool = True, ulysses_group=None):
+                 eps: float = 1e-6, compact: bool = True, ulysses_group=None, switch_chunks: int | None = None):
         import torch.distributed as dist
         self.g = g
         self.pg: PaddedGrid = pad_grid(g)
@@ -164,6 +164,21 @@ class SkiparseBlock:
             b = pgs.scatter[g2t]                             # padded TSA row <- compact GSA row
             self._fused = (row_move(a, pt.n_seq * pt.cap, pgs.cap, pt.cap),
                            row_move(b, pgs.n_seq * pgs.cap, pt.L, pgs.cap))
+
+        # N GPUs, NCCL transport: the switches run per head chunk on a communication stream,
+        # overlapped with the attention of the next chunk (ssp_overlap.py); switch_chunks=1 keeps
+        # one all-to-all per switch without overlap, 0 the unfused reference-shaped path
+        self._overlap = None
+        if switch_chunks is None:
+            switch_chunks = next(c for c in (4, 2, 1) if heads % c == 0)
+        if (self.world > 1 and self.uly == 1 and transport == "native" and compact and not self.prologue
+                and d in (64, 128) and switch_chunks >= 1):
+            from .compact import compact_plan
+            from .ssp_overlap import SSPOverlapPlan
+            if self.plan_tsa is None:   # trivial grid: identity plans
+                full = compact_plan(torch.ones(self.local_rows, self.L, dtype=torch.bool, device=dev))
+                self.plan_tsa = self.plan_gsa = full
+            self._overlap = SSPOverlapPlan(self, switch_chunks)
 
         # N GPUs, transport "p2p": each switch is one pull over peer memory (K7, peer.py) whose
         # table folds expand -> switch -> compact; every rank builds every rank's plans
@@ -346,6 +361,10 @@ class SkiparseBlock:
         """x_tsa: this rank's (G*B, L, C) bf16 shard in the token-wise layout."""
         if self._scatter is not None:
             return self._call_scatter(x_tsa)
+        if self._overlap is not None:
+            from .compact import compact_rows
+            from .ssp_overlap import SSPOverlapBlock
+            return SSPOverlapBlock.apply(compact_rows(x_tsa, self.plan_tsa), self)
         if self._fused is not None:
             return self._call_fused(x_tsa)
         if self._peer is not None:

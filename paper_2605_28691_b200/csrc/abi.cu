@@ -18,6 +18,9 @@ int launch_bytes_to_bits(const uint8_t* valid, uint32_t* bits, int64_t n_rows, i
 int launch_bits_to_bytes(const uint32_t* bits, uint8_t* valid, int64_t n_rows, int64_t L,
                          cudaStream_t stream);
 int launch_invert_index(const int64_t* index, int64_t* inv, int64_t n, cudaStream_t stream);
+int launch_gather_chunks(const int64_t* index, const void* src, void* dst, int64_t n_rows, int64_t n_in_rows,
+                         int n_chunks, int64_t chunk_bytes, int64_t src_rs, int64_t src_cs, int64_t dst_rs,
+                         int64_t dst_cs, cudaStream_t stream);
 int launch_hif8_encode(const void* x, int dtype, int64_t n, const double* scale, int64_t group,
                        const double* table, uint8_t* codes, int* nonfinite, cudaStream_t stream);
 int launch_hif8_decode(const uint8_t* codes, int64_t n, const double* scale, int64_t group,
@@ -253,6 +256,24 @@ int osp_gather_rows(const void* src, void* dst, const int64_t* index, int64_t n_
   p.n_in_rows = n_in_rows;
   p.T = p.H = p.W = p.k = 1;
   return launch_permute(p, src, dst, n_out_rows, row_bytes, as_stream(stream));
+}
+
+int osp_gather_rows_chunked(const void* src, void* dst, const int64_t* index, int64_t n_out_rows,
+                            int64_t n_in_rows, int64_t n_chunks, int64_t chunk_bytes,
+                            int64_t src_row_stride, int64_t src_chunk_stride, int64_t dst_row_stride,
+                            int64_t dst_chunk_stride, void* stream) {
+  if (n_out_rows < 0 || n_in_rows < 0 || chunk_bytes < 0 || n_chunks < 0 || n_chunks > (1 << 20) ||
+      src_row_stride < 0 || src_chunk_stride < 0 || dst_row_stride < 0 || dst_chunk_stride < 0) {
+    set_error("negative sizes / strides");
+    return kValue;
+  }
+  if (n_out_rows && !index) {
+    set_error("missing index table");
+    return kValue;
+  }
+  return launch_gather_chunks(index, src, dst, n_out_rows, n_in_rows, static_cast<int>(n_chunks), chunk_bytes,
+                              src_row_stride, src_chunk_stride, dst_row_stride, dst_chunk_stride,
+                              as_stream(stream));
 }
 
 int osp_invert_index(const int64_t* index, int64_t* inv, int64_t n, void* stream) {

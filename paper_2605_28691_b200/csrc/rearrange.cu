@@ -248,6 +248,81 @@ int launch_permute(const MapParams& p, const void* src, void* dst, int64_t n_row
   return launch_permute_v<uint8_t>(p, src, dst, n_rows, row_bytes, stream);
 }
 
+// ------------------------------------------------------------------------- chunked table gather
+// dst row r, channel chunk c  <-  src row index[r], chunk c, for layouts that store the channel
+// chunks either inline (row stride = whole row, chunk stride = chunk width) or as separate
+// contiguous blocks (row stride = chunk width, chunk stride = rows x chunk width).  This is the
+// SSP switch's local step when the all-to-all runs per head chunk (overlapped with attention):
+// the unpack (+ compaction) of all received chunks into one row-major activation, and the pack of
+// a gradient into per-chunk send blocks.  index[r] < 0 (or >= n_in_rows) writes zeros.
+template <typename V>
+__global__ void __launch_bounds__(256) gather_chunks_warp(const int64_t* __restrict__ index,
+                                                          const uint8_t* __restrict__ src,
+                                                          uint8_t* __restrict__ dst, int64_t n_rows,
+                                                          int64_t n_in_rows, int n_chunks, int64_t chunk_vecs,
+                                                          int64_t src_rs, int64_t src_cs, int64_t dst_rs,
+                                                          int64_t dst_cs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < n_rows;
+       row += nwarps) {
+    int64_t s = __ldg(index + row);
+    if (s >= n_in_rows) s = -1;
+    for (int c = 0; c < n_chunks; ++c) {
+      V* out = reinterpret_cast<V*>(dst + c * dst_cs + row * dst_rs);
+      if (s < 0) {
+        V z;
+        memset(&z, 0, sizeof(V));
+        for (int64_t i = lane; i < chunk_vecs; i += 32) out[i] = z;
+        continue;
+      }
+      const V* in = reinterpret_cast<const V*>(src + c * src_cs + s * src_rs);
+      int64_t i = lane;
+      for (; i + 96 < chunk_vecs; i += 128) {
+        V a0 = __ldg(in + i), a1 = __ldg(in + i + 32), a2 = __ldg(in + i + 64), a3 = __ldg(in + i + 96);
+        out[i] = a0;
+        out[i + 32] = a1;
+        out[i + 64] = a2;
+        out[i + 96] = a3;
+      }
+      for (; i < chunk_vecs; i += 32) out[i] = __ldg(in + i);
+    }
+  }
+}
+
+template <typename V>
+static int launch_gather_chunks_v(const int64_t* index, const void* src, void* dst, int64_t n_rows,
+                                  int64_t n_in_rows, int n_chunks, int64_t chunk_bytes, int64_t src_rs,
+                                  int64_t src_cs, int64_t dst_rs, int64_t dst_cs, cudaStream_t stream) {
+  int64_t blocks = (n_rows + 7) / 8;
+  blocks = blocks < 148 * 32 ? blocks : 148 * 32;
+  if (blocks < 1) blocks = 1;
+  gather_chunks_warp<V><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+      index, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), n_rows, n_in_rows, n_chunks,
+      chunk_bytes / static_cast<int64_t>(sizeof(V)), src_rs, src_cs, dst_rs, dst_cs);
+  return check_cuda(cudaGetLastError(), "gather_chunks launch");
+}
+
+int launch_gather_chunks(const int64_t* index, const void* src, void* dst, int64_t n_rows, int64_t n_in_rows,
+                         int n_chunks, int64_t chunk_bytes, int64_t src_rs, int64_t src_cs, int64_t dst_rs,
+                         int64_t dst_cs, cudaStream_t stream) {
+  if (n_rows == 0 || chunk_bytes == 0 || n_chunks == 0) return kOk;
+  const uint64_t al = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
+                      static_cast<uint64_t>(chunk_bytes) | static_cast<uint64_t>(src_rs) |
+                      static_cast<uint64_t>(src_cs) | static_cast<uint64_t>(dst_rs) | static_cast<uint64_t>(dst_cs);
+  if ((al & 15) == 0)
+    return launch_gather_chunks_v<uint4>(index, src, dst, n_rows, n_in_rows, n_chunks, chunk_bytes, src_rs,
+                                         src_cs, dst_rs, dst_cs, stream);
+  if ((al & 3) == 0)
+    return launch_gather_chunks_v<uint32_t>(index, src, dst, n_rows, n_in_rows, n_chunks, chunk_bytes, src_rs,
+                                            src_cs, dst_rs, dst_cs, stream);
+  if ((al & 1) == 0)
+    return launch_gather_chunks_v<uint16_t>(index, src, dst, n_rows, n_in_rows, n_chunks, chunk_bytes, src_rs,
+                                            src_cs, dst_rs, dst_cs, stream);
+  return launch_gather_chunks_v<uint8_t>(index, src, dst, n_rows, n_in_rows, n_chunks, chunk_bytes, src_rs,
+                                         src_cs, dst_rs, dst_cs, stream);
+}
+
 // ------------------------------------------------------------------------- K5 masks
 // bits[row][w] bit i <=> the source token of (row, 32*w+i) is real (r < H0 and c < W0).
 // pattern: 0 original, 1 token-wise, 2 group-wise (anyres.py:92-96 with attention.py:121-125

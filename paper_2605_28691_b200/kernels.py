@@ -109,6 +109,36 @@ def gather_rows(x: torch.Tensor, index: torch.Tensor, n_out_rows: int) -> torch.
     return out
 
 
+def gather_rows_chunked(src: torch.Tensor, index: torch.Tensor, n_out_rows: int, n_chunks: int,
+                        src_chunked: bool, dst_chunked: bool, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Row gather between channel-chunked layouts.  A plain layout is (rows, C); a chunked one is
+    (n_chunks, rows, C / n_chunks) (every chunk a contiguous block).  dst row r = src row index[r]
+    (-1 = zeros), chunk by chunk; returns dst in the requested layout."""
+    L = _lib.lib()
+    _cuda(src, "src")
+    src = src.contiguous()
+    es = src.element_size()
+    if src_chunked:
+        nc, n_in, cc = src.shape
+        C = nc * cc
+    else:
+        n_in, C = src.reshape(-1, src.shape[-1]).shape
+        cc = C // n_chunks
+        nc = n_chunks
+    if nc != n_chunks or cc * nc != C:
+        raise ShapeError(f"channels {C} do not split into {n_chunks} chunks")
+    index = index.to(device=src.device, dtype=torch.int64).contiguous()
+    if out is None:
+        shape = (nc, n_out_rows, cc) if dst_chunked else (n_out_rows, C)
+        out = torch.empty(shape, dtype=src.dtype, device=src.device)
+    s_rs, s_cs = (cc * es, n_in * cc * es) if src_chunked else (C * es, cc * es)
+    d_rs, d_cs = (cc * es, n_out_rows * cc * es) if dst_chunked else (C * es, cc * es)
+    _lib.check(STATS.run('gather_rows', 1, lambda: L.osp_gather_rows_chunked(
+        src.data_ptr(), out.data_ptr(), index.data_ptr(), n_out_rows, n_in, nc, cc * es, s_rs, s_cs,
+        d_rs, d_cs, _lib.stream_ptr(src.device))))
+    return out
+
+
 def _ptr_array(ptrs) -> "ctypes.Array":
     import ctypes
     return (ctypes.c_void_p * len(ptrs))(*[int(p) for p in ptrs])

@@ -226,3 +226,67 @@ def test_ssp_x_ulysses_block_matches_one_gpu(lib, S, U, grid):
         assert len(r) == 4, r
         assert r[1] < 2e-2 and r[2] < 2e-2, r
         assert "pattern-switch" in r[3] and "ulysses-qkv" in r[3], r
+
+
+def _overlap_worker(rank, world, port, grid, chunks, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        host_a2a = dist.all_to_all_single
+
+        def a2a(out, inp, group=None):          # host-staged all-to-all (gloo), on the caller's stream
+            o = torch.empty(out.shape, dtype=out.dtype)
+            host_a2a(o, inp.cpu(), group=group)
+            out.copy_(o)
+
+        dist.all_to_all_single = a2a
+        from paper_2605_28691_b200 import GridShape
+        from paper_2605_28691_b200.block import SkiparseBlock
+        from paper_2605_28691_b200.ssp import CommLog
+        g = GridShape(*grid)
+        C, heads = 512, 4
+        log = CommLog()
+        ov = SkiparseBlock(g, heads, C, log=log, switch_chunks=chunks)
+        ref = SkiparseBlock(g, heads, C, switch_chunks=0)        # unfused: attend + pack/a2a/unpack
+        assert ov._overlap is not None and ov._overlap.nc == chunks and ref._overlap is None
+        torch.manual_seed(1 + rank)
+        x = torch.randn(ov.local_rows, ov.L, C, device="cuda").to(torch.bfloat16)
+        gy = torch.randn_like(x)
+        xa, xb = x.clone().requires_grad_(True), x.clone().requires_grad_(True)
+        ya, yb = ov(xa), ref(xb)
+        ya.backward(gy)
+        yb.backward(gy)
+        torch.cuda.synchronize()
+        same_y = torch.equal(ya, yb)
+        # dK, dV are bitwise repeatable; dQ's L2 reduction order is not, so dx is compared tightly
+        e_dx = ((xa.grad.float() - xb.grad.float()).abs().max() / xb.grad.float().abs().max()).item()
+        q.put((rank, same_y, e_dx, log.count("all_to_all")))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("grid,chunks", [((2, 10, 12, 2), 4), ((2, 8, 16, 2), 2), ((1, 17, 20, 4), 4),
+                                         ((2, 10, 12, 2), 1)])
+def test_two_rank_overlapped_switch_equals_unfused_block(lib, grid, chunks):
+    """The head-chunked switch (attention epilogue stores into the per-chunk send blocks, one
+    all-to-all per chunk on a comm stream, one K1 gather for unpack + compaction) equals the
+    unfused block (compact / attention / expand / pack / all-to-all / unpack) bit for bit in the
+    forward, with one logical all-to-all per switch."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overlap_worker, args=(r, 2, port, grid, chunks, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert len(r) == 4, r
+        _, same_y, e_dx, n_a2a = r
+        assert same_y
+        assert e_dx < 5e-3, e_dx
+        assert n_a2a == 4
