@@ -224,21 +224,37 @@ class SkiparseBlock:
             return self._g2t.apply(x)
         return ssp_switch(x, self.sub_grid, self.group, self.log, self.transport)
 
+    def _uly_moves(self, R: int):
+        """K1 row moves between Ulysses position blocks and whole subsequences: (n*R, L/U, X) with
+        rows (block j, subsequence r) <-> (R, L, X) with the U blocks of r concatenated."""
+        key = ("uly", R)
+        if key not in self.__dict__.setdefault("_moves", {}):
+            from .compact import row_move
+            n, Lu = self.uly, self.L_local
+            dev = self.W1.device
+            r = torch.arange(R, device=dev).view(R, 1, 1)
+            j = torch.arange(n, device=dev).view(1, n, 1)
+            p = torch.arange(Lu, device=dev).view(1, 1, Lu)
+            src = ((j * R + r) * Lu + p).reshape(-1)          # dst row (r, j, p) <- src (j, r, p)
+            gather = row_move(src, n * R * Lu, self.L, Lu)
+            scatter = row_move(gather.inv, R * self.L, Lu, self.L)
+            self._moves[key] = (gather, scatter)
+        return self._moves[key]
+
     def _ulysses_in(self, qkv):
         """(R, L/U, 3C) position block, all heads -> (R, L, 3C/U) all positions, my heads."""
+        from .compact import apply_move
         from .stack import _UlyssesQKV
         n = self.uly
         h = _UlyssesQKV.apply(qkv, n, self.uly_group, self.log)            # (n*R, L/U, 3C/n)
-        R = qkv.shape[0]
-        return h.view(n, R, self.L_local, -1).transpose(0, 1).reshape(R, self.L, -1)
+        return apply_move(h, self._uly_moves(qkv.shape[0])[0])
 
     def _ulysses_out(self, o):
         """(R, L, C/U) my heads -> (R, L/U, C) my position block, all heads."""
+        from .compact import apply_move
         from .stack import _UlyssesOut
-        n = self.uly
-        R = o.shape[0]
-        rows = o.view(R, n, self.L_local, -1).transpose(0, 1).reshape(n * R, self.L_local, -1)
-        return _UlyssesOut.apply(rows, n, self.uly_group, self.log)
+        rows = apply_move(o, self._uly_moves(o.shape[0])[1])               # (n*R, L/U, C/n)
+        return _UlyssesOut.apply(rows, self.uly, self.uly_group, self.log)
 
     def attend(self, x, W, bits, pattern=SparsePattern.TOKEN_WISE, compact_in=False, expand=True):
         """One attention application on this rank's shard.  compact_in: x already holds the

@@ -20,6 +20,7 @@
 #include "osp_internal.h"
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace osp {
 namespace {
@@ -29,6 +30,11 @@ constexpr int kBM = 128;
 constexpr int kBN = 128;
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// every kPolyEvery-th packed column pair of a full tile uses the polynomial exp2 (0 = never)
+#ifndef OSP_FWD_POLY
+#define OSP_FWD_POLY 4
+#endif
+constexpr int kPolyEvery = OSP_FWD_POLY;
 
 template <int D>
 struct FwdLayout {
@@ -377,53 +383,66 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       auto needs_rescale = [&](float m_new) {
         return (m_new > m_used) && (m_used == -INFINITY || (m_new - m_used) * c > kRescaleThreshold);
       };
-      // exp2 of the tile against the current max, P -> TMEM (bf16 over the S columns)
-      float ls0 = 0.f, ls1 = 0.f;
-      auto exps = [&](bool turn) {
+      // exp2 of the tile against the current max, P -> TMEM (bf16 over the S columns).  Scale and
+      // row sums run on packed fp32x2 (FFMA2 / FADD2); on tiles without masked keys every
+      // kPolyEvery-th column pair takes the FMA-pipe polynomial instead of MUFU.EX2, so one tile's
+      // exps need ~3/4 of the MUFU time and its softmax fits the other tile's MMA window.
+      float2 lsum = make_float2(0.f, 0.f);
+      auto exps = [&](bool turn, auto poly_tag) {
+        constexpr bool kPoly = decltype(poly_tag)::value;
         const float ms = (m_used == -INFINITY) ? 0.f : m_used * c;
-        ls0 = 0.f;
-        ls1 = 0.f;
+        const float2 c2 = make_float2(c, c), nms2 = make_float2(-ms, -ms);
+        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            float p0 = fmaf(__uint_as_float(s[cc][2 * i]), c, -ms);
-            float p1 = fmaf(__uint_as_float(s[cc][2 * i + 1]), c, -ms);
-            if (!(flags & 1)) {
-              p0 = ex2(p0);
-              p1 = ex2(p1);
+            const float2 x = __ffma2_rn(
+                make_float2(__uint_as_float(s[cc][2 * i]), __uint_as_float(s[cc][2 * i + 1])), c2, nms2);
+            float2 p;
+            if (kPoly && kPolyEvery > 0 && (i % kPolyEvery) == kPolyEvery - 1) {
+              p = exp2_poly2(x);
+            } else {
+              p.x = ex2(x.x);
+              p.y = ex2(x.y);
             }
-            ls0 += p0;
-            ls1 += p1;
-            pk[i] = pack_bf16(p0, p1);
+            if (i & 1) a1 = __fadd2_rn(a1, p);
+            else a0 = __fadd2_rn(a0, p);
+            pk[i] = pack_bf16(p.x, p.y);
           }
           if (turn && pingpong && cc == 3 && !(t == 1 && j == n_kv - 1))
             asm volatile("bar.arrive %0, 256;" ::"r"(next_turn) : "memory");
           tmem_st16(tS + cc * 16, pk);
         }
+        lsum = __fadd2_rn(a0, a1);
+      };
+      const bool full_tile = (w[0] & w[1] & w[2] & w[3]) == 0xFFFFFFFFu;
+      auto run_exps = [&](bool turn) {
+        if (full_tile) exps(turn, std::true_type{});
+        else exps(turn, std::false_type{});
       };
       if (__any_sync(0xFFFFFFFFu, m_used == -INFINITY)) {
         // no running max yet: exact row max first
         const float m_new = fmaxf(m_used, row_max());
         if (__any_sync(0xFFFFFFFFu, needs_rescale(m_new))) rescale(m_new);
         if (pingpong) named_bar_sync(my_turn, 256);
-        exps(true);
+        run_exps(true);
       } else {
         // Speculative: exponentiate against the running max straight away (values up to 2^8
         // above it are fine for bf16 P and the fp32 sums -- the lazy-rescale threshold) while
         // the row max is reduced off the MUFU critical path; a tile that overshoots by more is
         // rescaled and redone (rare once the max has settled).
         if (pingpong) named_bar_sync(my_turn, 256);
-        exps(true);
+        run_exps(true);
         const float m_new = fmaxf(m_used, row_max());
         if (__any_sync(0xFFFFFFFFu, needs_rescale(m_new))) {
           rescale(m_new);
-          exps(false);
+          run_exps(false);
         }
       }
       tmem_wait_st();
-      l += ls0 + ls1;
+      l += lsum.x + lsum.y;
       tc_fence_before();
       mbar_arrive(bar_p + t);
     }

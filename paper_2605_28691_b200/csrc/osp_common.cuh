@@ -43,13 +43,29 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the thread sleeps until the phase completes (or the hint
+// elapses) instead of re-issuing the probe, so a waiting warp leaves its scheduler's issue
+// slots to the warps that compute.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+      "selp.b32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
 // Blocking wait with a watchdog: a pipeline-protocol bug traps (~20 s) instead of hanging
-// the GPU.
+// the GPU.  The clock is read only every 64 probes (the probes themselves sleep).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try_wait(bar, parity)) {
-    if (clock64() - t0 > (40LL << 30)) __trap();
+  for (uint32_t n = 1; !mbar_try_wait_sleep(bar, parity); ++n) {
+    if ((n & 63u) == 0u && clock64() - t0 > (40LL << 30)) __trap();
   }
 }
 
@@ -356,6 +372,25 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
+}
+// 2^x for a pair on the FMA / integer pipes (no MUFU): round-to-nearest split x = n + f with the
+// 1.5*2^23 magic constant (|f| <= 1/2), degree-3 minimax polynomial for 2^f on packed fp32x2
+// (FFMA2 / FADD2), and n added into the exponent field with one integer multiply-add per lane.
+// Inputs are clamped below at -127 (the result is then ~2^-127, not 0: callers use it only on
+// tiles without masked keys).  Relative error ~1e-4, well below bf16's 2^-9 rounding of P.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  constexpr float kMagic = 12582912.f;
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
+  const float2 n = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
+  const float2 f = __ffma2_rn(n, make_float2(-1.f, -1.f), x);
+  float2 p = __ffma2_rn(f, make_float2(0.05500893f, 0.05500893f), make_float2(0.24221099f, 0.24221099f));
+  p = __ffma2_rn(p, f, make_float2(0.69328293f, 0.69328293f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  // (bits(t) << 23) == n << 23 (bits(t) = 0x4B400000 + n, whose high part shifts out)
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 }  // namespace osp

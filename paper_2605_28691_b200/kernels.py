@@ -109,15 +109,33 @@ def gather_rows(x: torch.Tensor, index: torch.Tensor, n_out_rows: int) -> torch.
     return out
 
 
+def gather_chunks(src: torch.Tensor, dst: torch.Tensor, index: torch.Tensor, n_out_rows: int, n_in_rows: int,
+                  n_chunks: int, chunk_elems: int, src_row_stride: int, src_chunk_stride: int,
+                  dst_row_stride: int, dst_chunk_stride: int) -> torch.Tensor:
+    """Raw chunked row gather (element strides from the tensors' data pointers, which may be views):
+    for r < n_out_rows, c < n_chunks: dst[c*dcs + r*drs : +chunk] = src[c*scs + index[r]*srs : +chunk]
+    (index[r] < 0 -> zeros)."""
+    L = _lib.lib()
+    _cuda(src, "src")
+    _cuda(dst, "dst")
+    if src.dtype != dst.dtype:
+        raise ShapeError("src and dst dtypes differ")
+    es = src.element_size()
+    index = index.to(device=src.device, dtype=torch.int64).contiguous()
+    _lib.check(STATS.run('gather_rows', 1, lambda: L.osp_gather_rows_chunked(
+        src.data_ptr(), dst.data_ptr(), index.data_ptr(), n_out_rows, n_in_rows, n_chunks, chunk_elems * es,
+        src_row_stride * es, src_chunk_stride * es, dst_row_stride * es, dst_chunk_stride * es,
+        _lib.stream_ptr(src.device))))
+    return dst
+
+
 def gather_rows_chunked(src: torch.Tensor, index: torch.Tensor, n_out_rows: int, n_chunks: int,
                         src_chunked: bool, dst_chunked: bool, out: torch.Tensor | None = None) -> torch.Tensor:
     """Row gather between channel-chunked layouts.  A plain layout is (rows, C); a chunked one is
     (n_chunks, rows, C / n_chunks) (every chunk a contiguous block).  dst row r = src row index[r]
     (-1 = zeros), chunk by chunk; returns dst in the requested layout."""
-    L = _lib.lib()
     _cuda(src, "src")
     src = src.contiguous()
-    es = src.element_size()
     if src_chunked:
         nc, n_in, cc = src.shape
         C = nc * cc
@@ -127,15 +145,51 @@ def gather_rows_chunked(src: torch.Tensor, index: torch.Tensor, n_out_rows: int,
         nc = n_chunks
     if nc != n_chunks or cc * nc != C:
         raise ShapeError(f"channels {C} do not split into {n_chunks} chunks")
-    index = index.to(device=src.device, dtype=torch.int64).contiguous()
     if out is None:
         shape = (nc, n_out_rows, cc) if dst_chunked else (n_out_rows, C)
         out = torch.empty(shape, dtype=src.dtype, device=src.device)
-    s_rs, s_cs = (cc * es, n_in * cc * es) if src_chunked else (C * es, cc * es)
-    d_rs, d_cs = (cc * es, n_out_rows * cc * es) if dst_chunked else (C * es, cc * es)
-    _lib.check(STATS.run('gather_rows', 1, lambda: L.osp_gather_rows_chunked(
-        src.data_ptr(), out.data_ptr(), index.data_ptr(), n_out_rows, n_in, nc, cc * es, s_rs, s_cs,
-        d_rs, d_cs, _lib.stream_ptr(src.device))))
+    s_rs, s_cs = (cc, n_in * cc) if src_chunked else (C, cc)
+    d_rs, d_cs = (cc, n_out_rows * cc) if dst_chunked else (C, cc)
+    return gather_chunks(src, out, index, n_out_rows, n_in, nc, cc, s_rs, s_cs, d_rs, d_cs)
+
+
+_IOTA: dict = {}
+
+
+def iota_index(n: int, device) -> torch.Tensor:
+    key = (n, str(device))
+    if key not in _IOTA:
+        _IOTA[key] = torch.arange(n, dtype=torch.int64, device=device)
+    return _IOTA[key]
+
+
+def ulysses_pack_qkv(qkv: torch.Tensor, n: int) -> torch.Tensor:
+    """(R, L, 3C) packed [q|k|v], all heads -> (n, R*L, 3C/n) send blocks: block j holds peer j's
+    channel slice of q, k and v (three K1 chunked gathers; replaces view/permute/contiguous)."""
+    R, L, C3 = qkv.shape
+    C = C3 // 3
+    Cn = C // n
+    rows = R * L
+    src = qkv.contiguous()
+    out = torch.empty((n, rows, 3 * Cn), dtype=qkv.dtype, device=qkv.device)
+    idx = iota_index(rows, qkv.device)
+    for t in range(3):     # q, k, v part: src chunk j = columns t*C + j*Cn, dst chunk j = block j, cols t*Cn
+        gather_chunks(src.view(-1)[t * C:], out.view(-1)[t * Cn:], idx, rows, rows, n, Cn, C3, Cn,
+                      3 * Cn, rows * 3 * Cn)
+    return out
+
+
+def ulysses_unpack_qkv(blocks: torch.Tensor, n: int) -> torch.Tensor:
+    """Adjoint of ulysses_pack_qkv: (n, R*L, 3C/n) -> (R*L, 3C)."""
+    _, rows, C3n = blocks.shape
+    Cn = C3n // 3
+    C = n * Cn
+    src = blocks.contiguous()
+    out = torch.empty((rows, 3 * C), dtype=blocks.dtype, device=blocks.device)
+    idx = iota_index(rows, blocks.device)
+    for t in range(3):
+        gather_chunks(src.view(-1)[t * Cn:], out.view(-1)[t * C:], idx, rows, rows, n, Cn, 3 * Cn, rows * 3 * Cn,
+                      3 * C, Cn)
     return out
 
 

@@ -44,7 +44,7 @@ def ulysses_qkv_to_heads(qkv_local: torch.Tensor, n: int, group=None, log: CommL
     import torch.distributed as dist
     R, L, C3 = qkv_local.shape
     C = C3 // 3
-    send = qkv_local.view(R, L, 3, n, C // n).permute(3, 0, 1, 2, 4).contiguous()
+    send = kernels.ulysses_pack_qkv(qkv_local, n)           # (n, R*L, 3C/n), K1 chunked gathers
     recv = torch.empty_like(send)
     dist.all_to_all_single(recv, send, group=group)
     if log is not None:
@@ -61,7 +61,10 @@ def ulysses_out_to_rows(o_heads: torch.Tensor, n: int, group=None, log: CommLog 
     dist.all_to_all_single(recv, o_heads.contiguous(), group=group)
     if log is not None:
         log.record("all_to_all", o_heads.numel(), "ulysses-out", o_heads.numel() * o_heads.element_size())
-    return recv.view(n, R, L, Cn).permute(1, 2, 0, 3).reshape(R, L, n * Cn)
+    # (n, R*L, C/n) head blocks -> (R*L, C) rows: one K1 chunked gather
+    out = kernels.gather_rows_chunked(recv.view(n, R * L, Cn), kernels.iota_index(R * L, recv.device), R * L, n,
+                                      True, False)
+    return out.view(R, L, n * Cn)
 
 
 class _UlyssesQKV(torch.autograd.Function):
@@ -81,9 +84,8 @@ class _UlyssesQKV(torch.autograd.Function):
         dist.all_to_all_single(recv, g.contiguous(), group=ctx.group)
         if ctx.log is not None:
             ctx.log.record("all_to_all", g.numel(), "ulysses-qkv-bwd", g.numel() * g.element_size())
-        Cn = C3n // 3
-        out = recv.view(n, R, L, 3, Cn).permute(1, 2, 3, 0, 4).reshape(R, L, 3 * n * Cn)
-        return out, None, None, None
+        out = kernels.ulysses_unpack_qkv(recv.view(n, R * L, C3n), n)
+        return out.view(R, L, -1), None, None, None
 
 
 class _UlyssesOut(torch.autograd.Function):
@@ -97,7 +99,8 @@ class _UlyssesOut(torch.autograd.Function):
         import torch.distributed as dist
         n = ctx.n
         R, L, C = g.shape
-        send = g.view(R, L, n, C // n).permute(2, 0, 1, 3).contiguous()
+        send = kernels.gather_rows_chunked(g.reshape(R * L, C), kernels.iota_index(R * L, g.device), R * L, n,
+                                           False, True)
         recv = torch.empty_like(send)
         dist.all_to_all_single(recv, send, group=ctx.group)
         if ctx.log is not None:

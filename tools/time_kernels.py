@@ -13,6 +13,7 @@ from paper_2605_28691_b200 import kernels
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg3")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--what", default="fwd,bwd")
 a = ap.parse_args()
 T, H, W, k, heads, d, _ = CONFIGS[a.config]
 k2 = k * k
@@ -25,7 +26,7 @@ q, kk, v = qkv[..., :C], qkv[..., C:2 * C], qkv[..., 2 * C:]
 do = torch.randn(n, L, C, device="cuda").bfloat16()
 sc = 1 / math.sqrt(d)
 fl = 4 * n * L * L * d * heads
-for name in ("fwd", "bwd"):
+for name in a.what.split(","):
     o, lse = kernels.attn_fwd(q, kk, v, heads, d, None, False, sc)
     ts = []
     for r in range(a.reps + 1):
