@@ -289,6 +289,10 @@ int osp_peer_barrier(const void* const* flag_blocks, int rank, int n, uint32_t e
 int osp_peer_gather(const void* const* srcs, int n_src, int64_t stride_rows, const int64_t* table,
                     int64_t n_rows, void* dst, int64_t row_bytes, void* stream);
 
+/* Profiling counters of instrumented builds (-DOSP_FWD_TIMING=1): copies n <= 64 uint64 into
+ * host_out (zeros in normal builds) and optionally resets them.  Not part of the hot path. */
+int osp_debug_counters(uint64_t* host_out, int n, int reset);
+
 /* Self-test of the tcgen05 instruction forms (S = A B^T, O = bf16(S) V for one 128-row tile). */
 int osp_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,
                   int64_t head_dim, void* stream);

@@ -29,6 +29,8 @@ int launch_absmax(const void* x, int dtype, int64_t n, double* out, cudaStream_t
 int launch_hif8_scale(const double* amax, int64_t count, double target, double eps, double* scale,
                       cudaStream_t stream);
 
+int debug_counters(unsigned long long* host, int n, int reset);
+
 static thread_local std::string g_err;
 
 void set_error(const std::string& msg) { g_err = msg; }
@@ -573,6 +575,10 @@ int osp_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, int
   }
   return launch_qkv_project(x, w_t, out, rows, chan, out_stride, norm, gamma_q, gamma_k, eps, sumsq,
                             rope_table, t, h, w, k, pattern, batch, row_offset, as_stream(stream));
+}
+
+int osp_debug_counters(uint64_t* host_out, int n, int reset) {
+  return debug_counters(reinterpret_cast<unsigned long long*>(host_out), n, reset);
 }
 
 int osp_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,

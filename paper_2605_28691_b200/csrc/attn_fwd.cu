@@ -72,6 +72,13 @@ __device__ __forceinline__ bool bit_at(const uint32_t* bits, int words, int i) {
   return w < words && ((__ldg(bits + w) >> (i & 31)) & 1u);
 }
 
+// Phase timing (-DOSP_FWD_TIMING=1 builds only): per-phase clock64 sums of the first softmax
+// warp of each warpgroup and of the MMA issuer, read back with osp_debug_counters().
+#ifndef OSP_FWD_TIMING
+#define OSP_FWD_TIMING 0
+#endif
+__device__ unsigned long long g_fwd_counters[64];
+
 // Experiment switches (FwdArgs::flags) are compiled in only with -DOSP_FWD_EXPERIMENTS=1: the
 // softmax loop sits at its register budget, and even never-taken runtime branches cost time.
 #ifndef OSP_FWD_EXPERIMENTS
@@ -264,23 +271,47 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     mbar_wait(bar_q + 0, 0);
     mbar_wait(bar_q + 1, 0);
     tc_fence_after();
+#if OSP_FWD_TIMING
+    unsigned long long mt[4] = {0, 0, 0, 0};
+    long long m0 = clock64();
+#define OSP_MT(k) do { const long long _t = clock64(); mt[k] += _t - m0; m0 = _t; } while (0)
+#else
+#define OSP_MT(k) do { } while (0)
+#endif
     for (int j = 0; j < n_kv; ++j) {
       const int st = j & 1;
       const uint32_t ph = (j >> 1) & 1;
+#if OSP_FWD_TIMING
+      m0 = clock64();
+#endif
       mbar_wait(bar_kf + st, ph);
+      OSP_MT(0);
       tc_fence_after();
       qk(0, st, bar_s + 0, nullptr);
       if (j > 0) {
+#if OSP_FWD_TIMING
+        m0 = clock64();
+#endif
         mbar_wait(bar_p + 1, (j - 1) & 1);
+        OSP_MT(1);
         tc_fence_after();
         pv(1, (j - 1) & 1, j - 1 > 0, bar_ve + ((j - 1) & 1), nullptr, nullptr);
       }
       qk(1, st, bar_s + 1, bar_ke + st);
+#if OSP_FWD_TIMING
+      m0 = clock64();
+#endif
       mbar_wait(bar_vf + st, ph);
+      OSP_MT(2);
       mbar_wait(bar_p + 0, j & 1);
+      OSP_MT(3);
       tc_fence_after();
       pv(0, st, j > 0, nullptr, nullptr, nullptr);
     }
+#if OSP_FWD_TIMING
+    for (int k = 0; k < 4; ++k) atomicAdd(&g_fwd_counters[16 + k], mt[k]);
+    atomicAdd(&g_fwd_counters[20], static_cast<unsigned long long>(n_kv));
+#endif
     const int last = n_kv - 1;
     mbar_wait(bar_p + 1, last & 1);
     tc_fence_after();
@@ -326,12 +357,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     };
     uint32_t w_next[4];
     mask_words(0, w_next);
+#if OSP_FWD_TIMING
+    unsigned long long sp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long s0t = clock64();
+#define OSP_ST(k) do { const long long _t = clock64(); sp[k] += _t - s0t; s0t = _t; } while (0)
+#else
+#define OSP_ST(k) do { } while (0)
+#endif
     for (int j = 0; j < n_kv; ++j) {
+#if OSP_FWD_TIMING
+      s0t = clock64();
+#endif
       uint32_t w[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) w[i] = w_next[i];
       if (j + 1 < n_kv) mask_words(j + 1, w_next);
       mbar_wait(bar_s + t, j & 1);
+      OSP_ST(0);
       tc_fence_after();
       if (flags & 2) {
         tc_fence_before();
@@ -343,6 +385,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int cc = 0; cc < 4; ++cc) tmem_ld32(tS + cc * 32, s[cc]);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) tmem_wait_ld(s[cc]);
+      OSP_ST(1);
       if ((w[0] & w[1] & w[2] & w[3]) != 0xFFFFFFFFu) {
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc)
@@ -434,18 +477,28 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         // the row max is reduced off the MUFU critical path; a tile that overshoots by more is
         // rescaled and redone (rare once the max has settled).
         if (pingpong) named_bar_sync(my_turn, 256);
+        OSP_ST(2);
         run_exps(true);
+        OSP_ST(3);
         const float m_new = fmaxf(m_used, row_max());
         if (__any_sync(0xFFFFFFFFu, needs_rescale(m_new))) {
           rescale(m_new);
           run_exps(false);
         }
+        OSP_ST(4);
       }
       tmem_wait_st();
       l += lsum.x + lsum.y;
       tc_fence_before();
       mbar_arrive(bar_p + t);
+      OSP_ST(5);
     }
+#if OSP_FWD_TIMING
+    if (lane == 0 && wq == 0) {
+      for (int k = 0; k < 6; ++k) atomicAdd(&g_fwd_counters[t * 8 + k], sp[k]);
+      atomicAdd(&g_fwd_counters[t * 8 + 7], static_cast<unsigned long long>(n_kv));
+    }
+#endif
 
     // ---------------------------------------------------------------- epilogue
     mbar_wait(bar_o + t, 0);
@@ -544,6 +597,15 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
 }
 
 }  // namespace
+
+int debug_counters(unsigned long long* host, int n, int reset) {
+  if (n > 64) n = 64;
+  int rc = check_cuda(cudaMemcpyFromSymbol(host, g_fwd_counters, n * sizeof(unsigned long long)),
+                      "cudaMemcpyFromSymbol");
+  if (rc != kOk || !reset) return rc;
+  static const unsigned long long zeros[64] = {};
+  return check_cuda(cudaMemcpyToSymbol(g_fwd_counters, zeros, sizeof(zeros)), "cudaMemcpyToSymbol");
+}
 
 int launch_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
                     const AttnShape& s, int64_t q_stride, int64_t k_stride, int64_t v_stride,
