@@ -121,7 +121,24 @@ def _ulysses_worker(rank, world, port, q):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2605_28691_b200 import kernels
         from paper_2605_28691_b200.stack import _UlyssesOut, _UlyssesQKV
+
+        def gather_chunks(src, dst, index, n_out, n_in, nc, cc, srs, scs, drs, dcs):
+            # test-side restatement of the K1 chunked gather's element-stride contract
+            s, d = src.reshape(-1), dst.reshape(-1)
+            for r in range(n_out):
+                for c in range(nc):
+                    o = c * dcs + r * drs
+                    if index[r] < 0:
+                        d[o:o + cc] = 0
+                    else:
+                        i = c * scs + int(index[r]) * srs
+                        d[o:o + cc] = s[i:i + cc]
+            return dst
+
+        kernels.gather_chunks = gather_chunks
+        kernels._cuda = lambda t, name: None
         R, L, C = 3, 5, 8
         torch.manual_seed(0)
         full = torch.randn(world * R, L, 3 * C, dtype=torch.float64)   # all rows, all heads
