@@ -218,7 +218,12 @@ def _ncu_traffic(kernel: str):
         return None, None
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     total = 0.0
+    blocks = 0
     for line in Path(files[-1]).read_text().splitlines():
+        if line.startswith("----"):
+            blocks += 1
+            if blocks > 1:       # the first captured launch only (bytes per launch)
+                break
         m = re.match(r"dram__bytes_(read|write)\.sum = ([0-9.]+) (\w+)", line.strip())
         if m:
             total += float(m.group(2)) * units.get(m.group(3), 1)

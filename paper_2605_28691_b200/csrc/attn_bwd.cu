@@ -10,10 +10,13 @@
 //                   S^T = K Q^T, dP^T = V dO^T            (SS MMAs into TMEM)
 //                   P^T = exp2(S^T*c - lse2), dS^T = P^T (dP^T - delta)   (compute warps)
 //                   dV += P^T dO   (P^T read from TMEM),  dK += dS^T Q,  dQ_i = dS K
-//                 dV/dK accumulate in TMEM across the whole loop; dQ_i is drained from TMEM by
-//                 four writer warps with fp32 vector atomics into the workspace.
-//                 TMEM: [0,128) S^T/P^T, [128,256) dP^T then dQ_i, [256,256+D) dV,
-//                 [256+D, 256+2D) dK.
+//                 dV/dK accumulate in TMEM across the whole loop.  dQ_i is drained from TMEM by
+//                 four writer warps: d = 64 (attn_bwd_kernel) adds it with fp32 vector atomics
+//                 into the workspace; d = 128 (attn_bwd_v2_kernel, 64-query tiles) stages each
+//                 tile in shared memory and adds it with ONE cp.reduce.async.bulk (32 KB) into
+//                 the L2-resident accumulator.
+//                 TMEM (d = 64): [0,128) S^T/P^T, [128,256) dP^T then dQ_i, [256,256+D) dV,
+//                 [256+D, 256+2D) dK; the d = 128 layout is described at attn_bwd_v2_kernel.
 //   3. finalize : dq = bf16(scale * dq_acc).
 #include "osp_common.cuh"
 #include "osp_internal.h"

@@ -14,6 +14,10 @@
 //   warps 4-7   softmax for query tile 0, warps 8-11 for tile 1: one thread per row,
 //               online softmax in the log2 domain, lazy O rescaling (only when the running
 //               max grows by > 2^8), P written back into the S columns as packed bf16.
+//               Per tile: load S, exact row max, (rare) O rescale, then the exp phase -- the
+//               two warpgroups take turns on the SM's MUFU, so it holds only scale, exp2
+//               (MUFU or, for ~1/3 of the columns, an FMA-pipe polynomial), bf16 pack and the
+//               TMEM store -- then P is handed to the MMA and the row sum is added.
 // MMA order per key tile j: QK0_j, PV1_{j-1}, QK1_j, PV0_j, so one tile's softmax overlaps
 // the other tile's tensor-core work.
 #include "osp_common.cuh"
@@ -32,9 +36,18 @@ constexpr float kLn2 = 0.69314718055994530942f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // every kPolyEvery-th packed column pair of a full tile uses the polynomial exp2 (0 = never)
 #ifndef OSP_FWD_POLY
-#define OSP_FWD_POLY 4
+#define OSP_FWD_POLY 3
 #endif
 constexpr int kPolyEvery = OSP_FWD_POLY;
+// bf16 P by truncation (one PRMT per pair on the ALU pipe) instead of F2FP round-to-nearest; the
+// row sum l then adds the truncated values, so O / l stays an exactly normalised combination
+#ifndef OSP_FWD_TRUNC
+#define OSP_FWD_TRUNC 0
+#endif
+// serialise the two softmax warpgroups' exp phases (1) or let them overlap (0)
+#ifndef OSP_FWD_PINGPONG
+#define OSP_FWD_PINGPONG 1
+#endif
 
 template <int D>
 struct FwdLayout {
@@ -336,7 +349,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // finishes within the window the other tile's MMAs cover, instead of both running at half
     // speed.  Warpgroup 1 opens the first turn for warpgroup 0.
     const uint32_t my_turn = 2 + t, next_turn = 3 - t;
-    const bool pingpong = !(flags & 4);  // experiment 4: no exp-phase serialisation
+    const bool pingpong = OSP_FWD_PINGPONG && !(flags & 4);  // experiment 4: no exp-phase serialisation
     if (t == 1 && pingpong) asm volatile("bar.arrive %0, 256;" ::"r"(2u) : "memory");
 
     float m_used = -INFINITY;
@@ -426,16 +439,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       auto needs_rescale = [&](float m_new) {
         return (m_new > m_used) && (m_used == -INFINITY || (m_new - m_used) * c > kRescaleThreshold);
       };
-      // exp2 of the tile against the current max, P -> TMEM (bf16 over the S columns).  Scale and
-      // row sums run on packed fp32x2 (FFMA2 / FADD2); on tiles without masked keys every
-      // kPolyEvery-th column pair takes the FMA-pipe polynomial instead of MUFU.EX2, so one tile's
-      // exps need ~3/4 of the MUFU time and its softmax fits the other tile's MMA window.
-      float2 lsum = make_float2(0.f, 0.f);
+      // The exp phase is the serialised resource (the two warpgroups take turns on the SM's
+      // MUFU), so it holds only what must run in it: scale (FFMA2), exp2, bf16 pack, P -> TMEM.
+      // The row max runs before the turn and the row sum after P is handed over, both while the
+      // other warpgroup exponentiates.  On tiles without masked keys every kPolyEvery-th column
+      // pair takes the FMA-pipe polynomial instead of MUFU.EX2.  p overwrites s in place (fp32)
+      // for the row sum.
       auto exps = [&](bool turn, auto poly_tag) {
         constexpr bool kPoly = decltype(poly_tag)::value;
         const float ms = (m_used == -INFINITY) ? 0.f : m_used * c;
         const float2 c2 = make_float2(c, c), nms2 = make_float2(-ms, -ms);
-        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
           uint32_t pk[16];
@@ -450,47 +463,46 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               p.x = ex2(x.x);
               p.y = ex2(x.y);
             }
-            if (i & 1) a1 = __fadd2_rn(a1, p);
-            else a0 = __fadd2_rn(a0, p);
-            pk[i] = pack_bf16(p.x, p.y);
+            s[cc][2 * i] = __float_as_uint(p.x);
+            s[cc][2 * i + 1] = __float_as_uint(p.y);
+            pk[i] = OSP_FWD_TRUNC ? pack_bf16_trunc(p.x, p.y) : pack_bf16(p.x, p.y);
           }
           if (turn && pingpong && cc == 3 && !(t == 1 && j == n_kv - 1))
             asm volatile("bar.arrive %0, 256;" ::"r"(next_turn) : "memory");
           tmem_st16(tS + cc * 16, pk);
         }
-        lsum = __fadd2_rn(a0, a1);
       };
-      const bool full_tile = (w[0] & w[1] & w[2] & w[3]) == 0xFFFFFFFFu;
-      auto run_exps = [&](bool turn) {
-        if (full_tile) exps(turn, std::true_type{});
-        else exps(turn, std::false_type{});
-      };
-      if (__any_sync(0xFFFFFFFFu, m_used == -INFINITY)) {
-        // no running max yet: exact row max first
-        const float m_new = fmaxf(m_used, row_max());
-        if (__any_sync(0xFFFFFFFFu, needs_rescale(m_new))) rescale(m_new);
-        if (pingpong) named_bar_sync(my_turn, 256);
-        run_exps(true);
-      } else {
-        // Speculative: exponentiate against the running max straight away (values up to 2^8
-        // above it are fine for bf16 P and the fp32 sums -- the lazy-rescale threshold) while
-        // the row max is reduced off the MUFU critical path; a tile that overshoots by more is
-        // rescaled and redone (rare once the max has settled).
-        if (pingpong) named_bar_sync(my_turn, 256);
-        OSP_ST(2);
-        run_exps(true);
-        OSP_ST(3);
-        const float m_new = fmaxf(m_used, row_max());
-        if (__any_sync(0xFFFFFFFFu, needs_rescale(m_new))) {
-          rescale(m_new);
-          run_exps(false);
-        }
-        OSP_ST(4);
-      }
+      // Exact running max before the exps (off the MUFU turn).  The rescale of O, when the max
+      // grew by more than 2^kRescaleThreshold, is legal here: PV_{j-1} of this tile is complete.
+      const float m_new = fmaxf(m_used, row_max());
+      if (__any_sync(0xFFFFFFFFu, needs_rescale(m_new))) rescale(m_new);
+      if (pingpong) named_bar_sync(my_turn, 256);
+      OSP_ST(2);
+      if ((w[0] & w[1] & w[2] & w[3]) == 0xFFFFFFFFu) exps(true, std::true_type{});
+      else exps(true, std::false_type{});
+      OSP_ST(3);
       tmem_wait_st();
-      l += lsum.x + lsum.y;
       tc_fence_before();
       mbar_arrive(bar_p + t);
+      OSP_ST(4);
+      {
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+        if (OSP_FWD_TRUNC) {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) s[cc][i] &= 0xFFFF0000u;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          a0 = __fadd2_rn(a0, make_float2(__uint_as_float(s[0][2 * i]), __uint_as_float(s[0][2 * i + 1])));
+          a1 = __fadd2_rn(a1, make_float2(__uint_as_float(s[1][2 * i]), __uint_as_float(s[1][2 * i + 1])));
+          a2 = __fadd2_rn(a2, make_float2(__uint_as_float(s[2][2 * i]), __uint_as_float(s[2][2 * i + 1])));
+          a3 = __fadd2_rn(a3, make_float2(__uint_as_float(s[3][2 * i]), __uint_as_float(s[3][2 * i + 1])));
+        }
+        const float2 t2 = __fadd2_rn(__fadd2_rn(a0, a1), __fadd2_rn(a2, a3));
+        l += t2.x + t2.y;
+      }
       OSP_ST(5);
     }
 #if OSP_FWD_TIMING

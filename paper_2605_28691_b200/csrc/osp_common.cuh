@@ -61,10 +61,13 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t pari
 }
 // Blocking wait with a watchdog: a pipeline-protocol bug traps (~20 s) instead of hanging
 // the GPU.  The clock is read only every 64 probes (the probes themselves sleep).
+#ifndef OSP_MBAR_SLEEP
+#define OSP_MBAR_SLEEP 1
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const long long t0 = clock64();
-  for (uint32_t n = 1; !mbar_try_wait_sleep(bar, parity); ++n) {
+  for (uint32_t n = 1; !(OSP_MBAR_SLEEP ? mbar_try_wait_sleep(bar, parity) : mbar_try_wait(bar, parity)); ++n) {
     if ((n & 63u) == 0u && clock64() - t0 > (40LL << 30)) __trap();
   }
 }
@@ -371,6 +374,12 @@ __device__ __forceinline__ float ex2(float x) {
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// bf16x2 by truncation: the high halves of two fp32 words, one PRMT (ALU pipe)
+__device__ __forceinline__ uint32_t pack_bf16_trunc(float lo, float hi) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(__float_as_uint(lo)), "r"(__float_as_uint(hi)));
   return r;
 }
 // 2^x for a pair on the FMA / integer pipes (no MUFU): round-to-nearest split x = n + f with the

@@ -110,3 +110,65 @@ def test_block_fwd_bwd_matches_f64(lib, name, parity_record):
         e = errors(y.cpu(), torch.from_numpy(want))
         extra["y_vs_numpy_oracle"] = e
     _check(name, (y, dx), res["f64"], res["bf16"], parity_record, extra)
+
+
+def _orig_tables(g):
+    """(o2t flat table of the padded grid, pad mask flat) from the oracle (reference-pinned)."""
+    og = O.Grid(g.t, g.h, g.w, g.k)
+    pg = O.padded_grid(og)
+    o2t = torch.from_numpy(np.ascontiguousarray(O.map_table("orig_to_tsa", pg, 1).reshape(-1)))
+    mask = torch.from_numpy(np.ascontiguousarray(O.pad_mask(og).reshape(-1))) if pg != og else \
+        torch.ones(og.seq_len, dtype=torch.bool)
+    return o2t, mask
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_block_original_layout_fwd_bwd_matches_f64(lib, name, parity_record):
+    """SkiparseBlock.forward_original -- what bench.py times at N=1 (orig -> TSA -> GSA -> orig:
+    one K1 gather into compact TSA rows, both rearranges after the attention applications stored
+    by the attention epilogues, dO gathered in the backward's Delta pre-pass) -- whole output and
+    input gradient against the float64 block on the oracle's pad + orig_to_tsa tables."""
+    import paper_2605_28691_b200 as P
+    from paper_2605_28691_b200.block import SkiparseBlock
+    torch.backends.cuda.matmul.allow_tf32 = False
+    T, H, W, k, heads, d = CASES[name]
+    g = P.GridShape(T, H, W, k)
+    C = heads * d
+    blk = SkiparseBlock(g, heads, C)
+    S = T * H * W
+    gen = torch.Generator(device="cuda").manual_seed(77)
+    x = torch.randn(1, S, C, generator=gen, device="cuda").to(torch.bfloat16)
+    gy = torch.randn(1, S, C, generator=gen, device="cuda").to(torch.bfloat16)
+    xk = x.clone().requires_grad_(True)
+    y = blk.forward_original(xk)
+    y.backward(gy)
+    torch.cuda.synchronize()
+    dev = torch.device("cuda")
+    o2t, mask = (t.to(dev) for t in _orig_tables(g))
+    Sp = o2t.numel()
+
+    def to_tsa(t):                       # (1, S, C) unpadded -> (k^2, L, C) token-wise, pads 0
+        pad = torch.zeros(Sp, C, dtype=t.dtype, device=dev)
+        pad[mask] = t.reshape(S, C)
+        return pad[o2t].view(blk.local_rows, blk.L, C)
+
+    def to_orig(t):                      # adjoint / inverse of to_tsa on the real rows
+        pad = torch.empty(Sp, C, dtype=t.dtype, device=dev)
+        pad[o2t] = t.reshape(Sp, C)
+        return pad[mask].view(1, S, C)
+
+    t2g, g2t = block_tables(blk.grid)
+    vt, vg = layout_valid(g)
+    vt = None if vt is None else vt.to(dev)
+    vg = None if vg is None else vg.to(dev)
+    res = {}
+    for mode in ("f64", "bf16"):
+        ref = BlockRef(t2g.to(dev), g2t.to(dev), vt, vg, blk.W1.double(), blk.W2.double(), heads, mode)
+        yr, cache = ref.forward(to_tsa(x))
+        dxr = ref.backward(cache, to_tsa(gy))
+        del cache
+        res[mode] = (to_orig(yr), to_orig(dxr))
+    extra = {"config": {"grid": [T, H, W], "k": k, "heads": heads, "head_dim": d,
+                        "padded_grid": [blk.grid.t, blk.grid.h, blk.grid.w], "subseq_len": blk.L},
+             "path": "SkiparseBlock.forward_original (the benched N=1 step, orig -> orig), whole tensors"}
+    _check(name + "_orig", (y.detach(), xk.grad), res["f64"], res["bf16"], parity_record, extra)

@@ -6,7 +6,7 @@
 
 using namespace osp;
 
-template <bool ST>
+template <bool ST, bool BATCH = false>
 __global__ void __launch_bounds__(512, 1) tmem_kernel(int iters, unsigned long long* cycles, float* sink) {
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
@@ -23,6 +23,16 @@ __global__ void __launch_bounds__(512, 1) tmem_kernel(int iters, unsigned long l
   float acc = 0.f;
   long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
+    if (!ST && BATCH) {  // four 32-column loads in flight, one wait (the K2 softmax pattern)
+      uint32_t r[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tm + la + ((col0 + c * 32) & 511), r[c]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_wait_ld(r[c]);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc += __uint_as_float(r[c][0]) + __uint_as_float(r[c][31]);
+      continue;
+    }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       uint32_t r[32];
@@ -50,26 +60,27 @@ __global__ void __launch_bounds__(512, 1) tmem_kernel(int iters, unsigned long l
   }
 }
 
-template <bool ST>
+template <bool ST, bool BATCH = false>
 void run(int warps, int iters) {
   unsigned long long* d;
   float* s;
   cudaMalloc(&d, 8);
   cudaMalloc(&s, 4);
-  tmem_kernel<ST><<<148, warps * 32>>>(10, d, s);
+  tmem_kernel<ST, BATCH><<<148, warps * 32>>>(10, d, s);
   cudaDeviceSynchronize();
-  tmem_kernel<ST><<<148, warps * 32>>>(iters, d, s);
+  tmem_kernel<ST, BATCH><<<148, warps * 32>>>(iters, d, s);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long cyc;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
   const double bytes = double(warps) * 32 * 4 * 32 * 4 * iters;  // per CTA
-  printf("%s warps=%2d: %.1f bytes/clk/SM  (%s)\n", ST ? "tcgen05.st" : "tcgen05.ld", warps,
+  printf("%s%s warps=%2d: %.1f bytes/clk/SM  (%s)\n", ST ? "tcgen05.st" : "tcgen05.ld", BATCH ? " (4 in flight)" : "", warps,
          bytes / double(cyc), cudaGetErrorString(e));
   fflush(stdout);
 }
 
 int main() {
   for (int w : {4, 8, 16}) run<false>(w, 2000);
+  for (int w : {4, 8, 16}) run<false, true>(w, 2000);
   for (int w : {4, 8, 16}) run<true>(w, 2000);
   return 0;
 }
