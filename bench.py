@@ -270,16 +270,16 @@ def _comm_summary(log, steps: int) -> dict:
             "ulysses_bytes_per_rank_per_step": sum(e.bytes_per_rank for e in uly_ev) // steps}
 
 
-def _parity_summary(cfg: str):
+def _parity_summary(cfg: str, orig: bool = False):
     """Block parity errors recorded by tests/test_block_parity_gpu.py (committed copy in
     profiles/rNN_parity.json, newest round first) for this config."""
     import glob
     files = sorted(glob.glob(str(ROOT / "profiles" / "r*_parity.json")))
     for f in reversed(files):
         d = json.loads(Path(f).read_text())
-        e = d.get(f"block_{cfg}")
+        e = d.get(f"block_{cfg}_orig" if orig else f"block_{cfg}") or d.get(f"block_{cfg}")
         if e:
-            return {"source": Path(f).name, "rule": e.get("rule"),
+            return {"source": Path(f).name, "path": e.get("path"), "rule": e.get("rule"),
                     **{t: {k_: e[t][k_] for k_ in ("max_abs", "rel_l2", "budget_max_abs", "budget_rel_l2", "pass")}
                        for t in ("y", "dx") if t in e}}
     return None
@@ -592,7 +592,7 @@ def run_ours(args, world, rank, local_rank):
             "kernel_ms": kern, "kernel_share_of_step": share,
             "comm": comm,
             "clocks": clk.summary()}
-    par = _parity_summary(args.config)
+    par = _parity_summary(args.config, orig_step)
     if par:
         line["parity"] = par
     if world == 1 and not args.no_comparator:

@@ -39,10 +39,21 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define OSP_FWD_POLY 3
 #endif
 constexpr int kPolyEvery = OSP_FWD_POLY;
+// on tiles without masked keys the last kPolyChunks of the four 32-key chunks take the polynomial
+// exp2, computed before the warpgroup's MUFU turn (0-2)
+#ifndef OSP_FWD_POLY_CHUNKS
+#define OSP_FWD_POLY_CHUNKS 0
+#endif
+constexpr int kPolyChunks = OSP_FWD_POLY_CHUNKS;
 // bf16 P by truncation (one PRMT per pair on the ALU pipe) instead of F2FP round-to-nearest; the
 // row sum l then adds the truncated values, so O / l stays an exactly normalised combination
 #ifndef OSP_FWD_TRUNC
 #define OSP_FWD_TRUNC 0
+#endif
+// hand P over in two 64-key halves (PV issued as two K = 64 halves, the first under the second
+// half's exps) instead of one
+#ifndef OSP_FWD_SPLITPV
+#define OSP_FWD_SPLITPV 0
 #endif
 // serialise the two softmax warpgroups' exp phases (1) or let them overlap (0)
 #ifndef OSP_FWD_PINGPONG
@@ -77,7 +88,7 @@ struct FwdArgs {
   float scale_log2;
   int zero_invalid_q;
   int flags;  // debug experiments (OSP_FWD_FLAGS): 1 = no exp, 2 = softmax skeleton only,
-             // 4 = no exp-phase ping-pong, 8 = no K/V reloads
+             // 4 = no exp-phase ping-pong, 8 = no K/V reloads, 16 = no P store, 32 = no row sum
 };
 
 __device__ __forceinline__ bool bit_at(const uint32_t* bits, int words, int i) {
@@ -115,7 +126,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* bar_s = bars + 10;
   uint64_t* bar_p = bars + 12;
   uint64_t* bar_o = bars + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* bar_pb = bars + 16;  // second P half (OSP_FWD_SPLITPV)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -159,6 +171,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(bar_ve + i, 1);
       mbar_init(bar_s + i, 1);
       mbar_init(bar_p + i, 128);
+      mbar_init(bar_pb + i, 128);
       mbar_init(bar_o + i, 1);
     }
     fence_barrier_init();
@@ -268,17 +281,29 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (bar_b) tc_commit(bar_b);
       }
     };
-    auto pv = [&](int t, int st, bool acc, uint64_t* bar_a, uint64_t* bar_b, uint64_t* bar_c) {
+    // O_t += P_t V over keys [16*k0, 16*k1) of the tile
+    auto pv_part = [&](int t, int st, bool acc, int k0, int k1) {
       const uint32_t vb = v_base + st * Ly::kTile;
-      {
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)
-          mma_ts(tm + 256 + t * 128, tm + t * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
-                 kIdPV, (acc || kk > 0) ? 1u : 0u);
-        if (bar_a) tc_commit(bar_a);
-        if (bar_b) tc_commit(bar_b);
-        if (bar_c) tc_commit(bar_c);
+      for (int kk = k0; kk < k1; ++kk)
+        mma_ts(tm + 256 + t * 128, tm + t * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
+               kIdPV, (acc || kk > 0) ? 1u : 0u);
+    };
+    // waits for P_t (both halves, or the two halves one after the other) and issues PV_t
+    auto pv = [&](int t, int st, bool acc, uint32_t ph, uint64_t* bar_a, uint64_t* bar_b, uint64_t* bar_c) {
+      mbar_wait(bar_p + t, ph);
+      tc_fence_after();
+      if (OSP_FWD_SPLITPV) {
+        pv_part(t, st, acc, 0, kBN / 32);
+        mbar_wait(bar_pb + t, ph);
+        tc_fence_after();
+        pv_part(t, st, true, kBN / 32, kBN / 16);
+      } else {
+        pv_part(t, st, acc, 0, kBN / 16);
       }
+      if (bar_a) tc_commit(bar_a);
+      if (bar_b) tc_commit(bar_b);
+      if (bar_c) tc_commit(bar_c);
     };
     if (elect_one()) {
     mbar_wait(bar_q + 0, 0);
@@ -305,10 +330,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #if OSP_FWD_TIMING
         m0 = clock64();
 #endif
-        mbar_wait(bar_p + 1, (j - 1) & 1);
+        pv(1, (j - 1) & 1, j - 1 > 0, (j - 1) & 1, bar_ve + ((j - 1) & 1), nullptr, nullptr);
         OSP_MT(1);
-        tc_fence_after();
-        pv(1, (j - 1) & 1, j - 1 > 0, bar_ve + ((j - 1) & 1), nullptr, nullptr);
       }
       qk(1, st, bar_s + 1, bar_ke + st);
 #if OSP_FWD_TIMING
@@ -316,19 +339,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #endif
       mbar_wait(bar_vf + st, ph);
       OSP_MT(2);
-      mbar_wait(bar_p + 0, j & 1);
+      pv(0, st, j > 0, j & 1, nullptr, nullptr, nullptr);
       OSP_MT(3);
-      tc_fence_after();
-      pv(0, st, j > 0, nullptr, nullptr, nullptr);
     }
 #if OSP_FWD_TIMING
     for (int k = 0; k < 4; ++k) atomicAdd(&g_fwd_counters[16 + k], mt[k]);
     atomicAdd(&g_fwd_counters[20], static_cast<unsigned long long>(n_kv));
 #endif
     const int last = n_kv - 1;
-    mbar_wait(bar_p + 1, last & 1);
-    tc_fence_after();
-    pv(1, last & 1, last > 0, bar_ve + (last & 1), bar_o + 0, bar_o + 1);
+    pv(1, last & 1, last > 0, last & 1, bar_ve + (last & 1), bar_o + 0, bar_o + 1);
     }
     __syncwarp();
   }
@@ -391,6 +410,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (flags & 2) {
         tc_fence_before();
         mbar_arrive(bar_p + t);
+        mbar_arrive(bar_pb + t);
         continue;
       }
       uint32_t s[4][32];
@@ -445,47 +465,73 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // other warpgroup exponentiates.  On tiles without masked keys every kPolyEvery-th column
       // pair takes the FMA-pipe polynomial instead of MUFU.EX2.  p overwrites s in place (fp32)
       // for the row sum.
-      auto exps = [&](bool turn, auto poly_tag) {
-        constexpr bool kPoly = decltype(poly_tag)::value;
-        const float ms = (m_used == -INFINITY) ? 0.f : m_used * c;
-        const float2 c2 = make_float2(c, c), nms2 = make_float2(-ms, -ms);
+      const float2 c2 = make_float2(c, c);
+      float2 nms2;  // -(running max) * c, set once the max for this tile is final
+      // One 32-key chunk: scale, exp2 (MUFU, or with POLY the FMA-pipe polynomial), bf16 pack,
+      // P -> TMEM; p overwrites s in place (fp32) for the row sum.  MIX: inside a MUFU chunk every
+      // kPolyEvery-th pair still takes the polynomial (tiles without masked keys only).
+      auto chunk = [&](int cc, auto poly_tag, auto mix_tag, bool pass_turn) {
+        constexpr bool kAllPoly = decltype(poly_tag)::value;
+        constexpr bool kMix = decltype(mix_tag)::value;
+        uint32_t pk[16];
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 x = __ffma2_rn(
-                make_float2(__uint_as_float(s[cc][2 * i]), __uint_as_float(s[cc][2 * i + 1])), c2, nms2);
-            float2 p;
-            if (kPoly && kPolyEvery > 0 && (i % kPolyEvery) == kPolyEvery - 1) {
-              p = exp2_poly2(x);
-            } else {
-              p.x = ex2(x.x);
-              p.y = ex2(x.y);
-            }
-            s[cc][2 * i] = __float_as_uint(p.x);
-            s[cc][2 * i + 1] = __float_as_uint(p.y);
-            pk[i] = OSP_FWD_TRUNC ? pack_bf16_trunc(p.x, p.y) : pack_bf16(p.x, p.y);
+        for (int i = 0; i < 16; ++i) {
+          const float2 x = __ffma2_rn(
+              make_float2(__uint_as_float(s[cc][2 * i]), __uint_as_float(s[cc][2 * i + 1])), c2, nms2);
+          float2 p;
+          if (flags & 1) {  // experiment 1: no exp2 at all (timing only)
+            p = x;
+          } else if (kAllPoly || (kMix && kPolyEvery > 0 && (i % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1)) {
+            p = exp2_poly2(x);
+          } else {
+            p.x = ex2(x.x);
+            p.y = ex2(x.y);
           }
-          if (turn && pingpong && cc == 3 && !(t == 1 && j == n_kv - 1))
-            asm volatile("bar.arrive %0, 256;" ::"r"(next_turn) : "memory");
-          tmem_st16(tS + cc * 16, pk);
+          s[cc][2 * i] = __float_as_uint(p.x);
+          s[cc][2 * i + 1] = __float_as_uint(p.y);
+          pk[i] = OSP_FWD_TRUNC ? pack_bf16_trunc(p.x, p.y) : pack_bf16(p.x, p.y);
+        }
+        if (pass_turn && pingpong && !(t == 1 && j == n_kv - 1))
+          asm volatile("bar.arrive %0, 256;" ::"r"(next_turn) : "memory");
+        if (!(flags & 16)) tmem_st16(tS + cc * 16, pk);  // experiment 16: no P store (timing only)
+        if (OSP_FWD_SPLITPV && cc == 1) {  // keys 0-63 of P ready: PV's first half may run
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(bar_p + t);
         }
       };
       // Exact running max before the exps (off the MUFU turn).  The rescale of O, when the max
       // grew by more than 2^kRescaleThreshold, is legal here: PV_{j-1} of this tile is complete.
       const float m_new = fmaxf(m_used, row_max());
       if (__any_sync(0xFFFFFFFFu, needs_rescale(m_new))) rescale(m_new);
-      if (pingpong) named_bar_sync(my_turn, 256);
-      OSP_ST(2);
-      if ((w[0] & w[1] & w[2] & w[3]) == 0xFFFFFFFFu) exps(true, std::true_type{});
-      else exps(true, std::false_type{});
+      {
+        const float ms = (m_used == -INFINITY) ? 0.f : m_used * c;
+        nms2 = make_float2(-ms, -ms);
+      }
+      using T_ = std::true_type;
+      using F_ = std::false_type;
+      if ((w[0] & w[1] & w[2] & w[3]) == 0xFFFFFFFFu) {
+        // the last kPolyChunks chunks run on the FMA pipe BEFORE the MUFU turn, i.e. while the
+        // other warpgroup holds the MUFU; the rest on MUFU during this warpgroup's turn
+#pragma unroll
+        for (int cc = 4 - kPolyChunks; cc < 4; ++cc) chunk(cc, T_{}, F_{}, false);
+        if (pingpong) named_bar_sync(my_turn, 256);
+        OSP_ST(2);
+#pragma unroll
+        for (int cc = 0; cc < 4 - kPolyChunks; ++cc) chunk(cc, F_{}, T_{}, cc == 3 - kPolyChunks);
+      } else {
+        // masked keys need exact zeros: MUFU everywhere
+        if (pingpong) named_bar_sync(my_turn, 256);
+        OSP_ST(2);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) chunk(cc, F_{}, F_{}, cc == 3);
+      }
       OSP_ST(3);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(bar_p + t);
+      mbar_arrive(OSP_FWD_SPLITPV ? bar_pb + t : bar_p + t);
       OSP_ST(4);
-      {
+      if (!(flags & 32)) {  // experiment 32: no row sum (timing only)
         float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
         if (OSP_FWD_TRUNC) {
 #pragma unroll
