@@ -17,6 +17,7 @@ from dataclasses import dataclass
 import torch
 
 from . import kernels
+from .errors import ShapeError
 
 __all__ = ["CompactPlan", "compact_plan", "compact_rows", "expand_rows", "RowMove", "row_move",
            "GatherPlan", "gather_plan", "ScatterPlan", "scatter_plan"]
@@ -103,11 +104,21 @@ class RowMove:
     in_rows: int
 
 
+def _check_table(tab: torch.Tensor, n_rows: int, what: str) -> torch.Tensor:
+    """Range check of a row table once, when its plan is built (entries in [-1, n_rows)): the
+    kernels index with it unchecked."""
+    if tab.numel() and (int(tab.min()) < -1 or int(tab.max()) >= n_rows):
+        raise ShapeError(f"{what}: row index out of range [-1, {n_rows})")
+    return tab
+
+
 def row_move(src: torch.Tensor, n_in_total: int, out_rows: int, in_rows: int) -> RowMove:
-    src = src.to(torch.int64).contiguous()
+    src = _check_table(src.to(torch.int64).contiguous(), n_in_total, "row move")
     inv = torch.full((n_in_total,), -1, dtype=torch.int64, device=src.device)
     ok = src >= 0
     inv[src[ok]] = torch.nonzero(ok).view(-1)
+    if int((inv >= 0).sum()) != int(ok.sum()):
+        raise ShapeError("row move is not injective (its adjoint would be wrong)")
     return RowMove(src, inv, out_rows, in_rows)
 
 
@@ -143,7 +154,7 @@ def scatter_plan(out_index: torch.Tensor, n_seq: int, cap: int, n_out_rows: int,
                  out_shape: tuple) -> ScatterPlan:
     """out_index (n_seq*cap,) int64: destination row of every source row (-1 = none); the map
     must be injective."""
-    oi = out_index.to(torch.int64).reshape(-1)
+    oi = _check_table(out_index.to(torch.int64).reshape(-1), n_out_rows, "scatter plan")
     hit = torch.zeros(n_out_rows, dtype=torch.bool, device=oi.device)
     ok = oi >= 0
     hit[oi[ok]] = True
