@@ -264,13 +264,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // runs the control flow; one elected lane issues, so operands stay warp-uniform)
     constexpr uint32_t kIdQK = idesc_bf16(kBM, kBN, 0, 0);
     constexpr uint32_t kIdPV = idesc_bf16(kBM, D, 0, 1);
-    const uint32_t tm = __shfl_sync(0xFFFFFFFFu, tmem, 0);
+    const uint32_t tm_ = __shfl_sync(0xFFFFFFFFu, tmem, 0);
     const uint32_t q_base = smem_u32(sm + Ly::kQ);
     const uint32_t k_base = smem_u32(sm + Ly::kK);
     const uint32_t v_base = smem_u32(sm + Ly::kV);
+    // The bases go through an opaque move at every use, so the compiler re-derives the ~40
+    // descriptor / TMEM addresses with a few adds instead of hoisting them out of the key loop
+    // into registers the 64-register control-warp budget cannot hold (they spilled to local
+    // memory and every MMA group reloaded them).
+    auto opaque = [](uint32_t v) {
+      asm volatile("mov.b32 %0, %0;" : "+r"(v));
+      return v;
+    };
     auto qk = [&](int t, int st, uint64_t* bar_a, uint64_t* bar_b) {
-      const uint32_t qa = q_base + t * Ly::kTile;
-      const uint32_t kb = k_base + st * Ly::kTile;
+      const uint32_t qa = opaque(q_base) + t * Ly::kTile;
+      const uint32_t kb = opaque(k_base) + st * Ly::kTile;
+      const uint32_t tm = opaque(tm_);
       {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -284,7 +293,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     };
     // O_t += P_t V over keys [16*k0, 16*k1) of the tile
     auto pv_part = [&](int t, int st, bool acc, int k0, int k1) {
-      const uint32_t vb = v_base + st * Ly::kTile;
+      const uint32_t vb = opaque(v_base) + st * Ly::kTile;
+      const uint32_t tm = opaque(tm_);
 #pragma unroll
       for (int kk = k0; kk < k1; ++kk)
         mma_ts(tm + 256 + t * 128, tm + t * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),

@@ -1,5 +1,5 @@
 set -u
-O=gpurun_out/ab9
+O=gpurun_out/ab13
 mkdir -p $O
-bash tools/ab_libs.sh fwd cfg3 4 libs_exp/lib_pp_p3.so libs_exp/lib_nopp_p0.so libs_exp/lib_nopp_p8.so libs_exp/lib_nopp_p3.so > $O/ab.txt 2>&1
-bash tools/ab_libs.sh fwd cfg3k4 2 libs_exp/lib_pp_p3.so libs_exp/lib_nopp_p0.so libs_exp/lib_nopp_p8.so >> $O/ab.txt 2>&1
+OSP_LIB=libs_exp/lib_opq56.so timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -k attention > $O/tests.log 2>&1; echo "tests rc=$?"
+bash tools/ab_libs.sh fwd cfg3 4 libs_exp/lib_head.so libs_exp/lib_opq56.so > $O/ab.txt 2>&1
