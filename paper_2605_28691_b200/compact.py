@@ -126,12 +126,15 @@ class _Move(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, mv):
         ctx.mv = mv
+        ctx.in_shape = x.shape
         return _move(x, mv.src, mv.src.numel(), mv.out_rows)
 
     @staticmethod
     def backward(ctx, g):
         mv = ctx.mv
-        return _move(g.contiguous(), mv.inv, mv.inv.numel(), mv.in_rows), None
+        # returned in the input's own shape: a merely broadcast-compatible shape would make
+        # autograd reduce it (sum_to_size), a full extra pass over the activation
+        return _move(g.contiguous(), mv.inv, mv.inv.numel(), mv.in_rows).view(ctx.in_shape), None
 
 
 def apply_move(x: torch.Tensor, mv: RowMove) -> torch.Tensor:
