@@ -590,6 +590,12 @@ def run_ours(args, world, rank, local_rank):
             "roofline": roof,
             "flops_per_step_per_gpu": fl,
             "kernel_ms": kern, "kernel_share_of_step": share,
+            # SURVEY.md sec. 8d's targets count attention FLOPs only; the step also runs the
+            # reference's projection GEMMs (cuBLAS), so this is the step's tokens/s over the time of
+            # this library's attention kernels alone (K2 + K3 incl. prep / finalize), for comparison
+            "attention_only_tokens_per_s": (tokens_step / (sum(v["total_ms"] for n, v in kern.items()
+                                                               if n.startswith("attn")) / args.steps / 1e3)
+                                            if any(n.startswith("attn") for n in kern) else None),
             "comm": comm,
             "clocks": clk.summary()}
     par = _parity_summary(args.config, orig_step)
