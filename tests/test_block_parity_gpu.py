@@ -122,7 +122,16 @@ def _orig_tables(g):
     return o2t, mask
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+EXTRA = {
+    # odd, padded and k = 3 / 4 grids through the same benched path (not BASELINE configs)
+    "k3_pad": (2, 20, 30, 3, 2, 64),     # H, W -> 27, 36
+    "k4_pad": (3, 30, 20, 4, 2, 128),    # H, W -> 32, 32
+    "k2_odd": (1, 13, 17, 2, 1, 64),     # H, W -> 16, 20
+    "k2_T5": (5, 8, 12, 2, 4, 64),       # no padding, T > 1
+}
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", *EXTRA])
 def test_block_original_layout_fwd_bwd_matches_f64(lib, name, parity_record):
     """SkiparseBlock.forward_original -- what bench.py times at N=1 (orig -> TSA -> GSA -> orig:
     one K1 gather into compact TSA rows, both rearranges after the attention applications stored
@@ -131,7 +140,7 @@ def test_block_original_layout_fwd_bwd_matches_f64(lib, name, parity_record):
     import paper_2605_28691_b200 as P
     from paper_2605_28691_b200.block import SkiparseBlock
     torch.backends.cuda.matmul.allow_tf32 = False
-    T, H, W, k, heads, d = CASES[name]
+    T, H, W, k, heads, d = CASES[name] if name in CASES else EXTRA[name]
     g = P.GridShape(T, H, W, k)
     C = heads * d
     blk = SkiparseBlock(g, heads, C)
