@@ -424,6 +424,8 @@ def run_ours(args, world, rank, local_rank):
     # ---- device-resident timed region
     kernels.STATS.reset(timing=True)
     log.events.clear()
+    log.timed.clear()
+    log.timing = world > 1
     stream = torch.cuda.current_stream()
     gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[local_rank]) \
         if "CUDA_VISIBLE_DEVICES" in os.environ else local_rank
@@ -444,6 +446,11 @@ def run_ours(args, world, rank, local_rank):
     comm = _comm_summary(log, args.steps) if world > 1 else None   # the timed steps only
     if comm is not None:
         comm["ssp_transport"] = transport
+        # device time of the SSP all-to-alls (summed over chunks, per step); they run on a
+        # communication stream under the attention of the next head chunk, so this is not the
+        # exposed time
+        comm["all_to_all_device_ms_per_step"] = {k_: v / args.steps for k_, v in log.collective_ms().items()}
+    log.timing = False
     kernels.STATS.reset(timing=False)
     t = torch.tensor([ms], device=dev)
     if world > 1:

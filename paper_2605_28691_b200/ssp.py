@@ -46,10 +46,37 @@ class CommLog:
     """Collective ledger (ssp.py:45-63); additionally records bytes."""
 
     events: list = field(default_factory=list)
+    # device timing of the collectives (CUDA event pairs on the stream each runs on), enabled by
+    # the benchmark for its timed region; read with collective_ms() after a synchronize
+    timing: bool = False
+    timed: list = field(default_factory=list)
 
     def record(self, kind: str, payload_per_rank: int, label: str = "",
                bytes_per_rank: int = 0) -> None:
         self.events.append(CommEvent(kind, int(payload_per_rank), label, int(bytes_per_rank)))
+
+    def time_start(self, stream=None):
+        """Event pair around one collective issued on `stream` (default: the current stream);
+        None when timing is off."""
+        if not self.timing:
+            return None
+        import torch
+        stream = stream if stream is not None else torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        return (e0, e1, stream)
+
+    def time_end(self, tok, label: str) -> None:
+        if tok is not None:
+            tok[1].record(tok[2])
+            self.timed.append((label, tok[0], tok[1]))
+
+    def collective_ms(self) -> dict:
+        """Summed device time of the timed collectives per label (ms)."""
+        out: dict = {}
+        for label, e0, e1 in self.timed:
+            out[label] = out.get(label, 0.0) + e0.elapsed_time(e1)
+        return out
 
     def count(self, kind: str | None = None) -> int:
         return sum(1 for e in self.events if kind is None or e.kind == kind)
@@ -223,7 +250,10 @@ def _dist_switch(x: torch.Tensor, g: GridShape, group, log: CommLog | None,
         if n == 1:
             recv = send
         else:
+            tok = log.time_start() if log is not None else None
             dist.all_to_all_single(recv, send, group=group)
+            if log is not None:
+                log.time_end(tok, "pattern-switch-" + mode)
         if log is not None:
             log.record("all_to_all", send.numel(), "pattern-switch", send.numel() * send.element_size())
     else:

@@ -110,7 +110,10 @@ def _attn_chunks_then_a2a(qkv, plan: SSPOverlapPlan, lens, A, group, d, scale, l
         ev.record(S)
         with torch.cuda.stream(M):
             M.wait_event(ev)
+            tok = log.time_start(M) if log is not None else None
             _a2a(recv[c], send[c], group)
+            if log is not None:
+                log.time_end(tok, label)
     S.wait_stream(M)
     if log is not None:
         log.record("all_to_all", send.numel(), label, send.numel() * send.element_size())
@@ -128,7 +131,10 @@ def _a2a_chunks_then_attn_bwd(g_recv, qkv, send, lses, plan: SSPOverlapPlan, len
     evs = []
     with torch.cuda.stream(M):
         for c in range(plan.nc):
+            tok = log.time_start(M) if log is not None else None
             _a2a(g_send[c], g_recv[c], group)
+            if log is not None:
+                log.time_end(tok, label + "-bwd")
             ev = torch.cuda.Event()
             ev.record(M)
             evs.append(ev)

@@ -46,8 +46,10 @@ def ulysses_qkv_to_heads(qkv_local: torch.Tensor, n: int, group=None, log: CommL
     C = C3 // 3
     send = kernels.ulysses_pack_qkv(qkv_local, n)           # (n, R*L, 3C/n), K1 chunked gathers
     recv = torch.empty_like(send)
+    tok = log.time_start() if log is not None else None
     dist.all_to_all_single(recv, send, group=group)
     if log is not None:
+        log.time_end(tok, "ulysses-qkv")
         log.record("all_to_all", send.numel(), "ulysses-qkv", send.numel() * send.element_size())
     return recv.view(n * R, L, 3 * (C // n))
 
@@ -58,8 +60,10 @@ def ulysses_out_to_rows(o_heads: torch.Tensor, n: int, group=None, log: CommLog 
     NR, L, Cn = o_heads.shape
     R = NR // n
     recv = torch.empty_like(o_heads)
+    tok = log.time_start() if log is not None else None
     dist.all_to_all_single(recv, o_heads.contiguous(), group=group)
     if log is not None:
+        log.time_end(tok, "ulysses-out")
         log.record("all_to_all", o_heads.numel(), "ulysses-out", o_heads.numel() * o_heads.element_size())
     # (n, R*L, C/n) head blocks -> (R*L, C) rows: one K1 chunked gather
     out = kernels.gather_rows_chunked(recv.view(n, R * L, Cn), kernels.iota_index(R * L, recv.device), R * L, n,
