@@ -1,0 +1,6 @@
+"""osp.attention -> paper_2605_28691_b200.attention (numpy data mode, see osp/__init__.py)."""
+from paper_2605_28691_b200 import attention as _m
+
+from ._conv import export as _export
+
+_export(_m, globals())

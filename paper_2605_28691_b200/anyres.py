@@ -96,7 +96,7 @@ def pad_tensor(x, pg: PaddedGrid, pad_value: float = 0.0, pad_fill=None):
     """Embed an original-grid tensor into the padded grid (anyres.py:69-82):
     the K1 pad gather writes zeros to pad slots; a non-zero pad_value or the
     test-only pad_fill rows are then scattered into the pad slots."""
-    data = x.data if isinstance(x, SequenceTensor) else x
+    data = x.tensor if isinstance(x, SequenceTensor) else x
     if data.shape[1] != pg.original.seq_len:
         raise ShapeError(f"expected seq {pg.original.seq_len}, got {data.shape[1]}")
     p = pg.padded
@@ -114,7 +114,7 @@ def pad_tensor(x, pg: PaddedGrid, pad_value: float = 0.0, pad_fill=None):
 
 def strip_padding(x, pg: PaddedGrid):
     """Keep real tokens in original order (anyres.py:85-89)."""
-    data = x.data if isinstance(x, SequenceTensor) else x
+    data = x.tensor if isinstance(x, SequenceTensor) else x
     if data.shape[1] != pg.padded.seq_len:
         raise ShapeError(f"expected padded seq {pg.padded.seq_len}, got {data.shape[1]}")
     p = pg.padded

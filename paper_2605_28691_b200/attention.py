@@ -62,8 +62,8 @@ def packed_projection(chan: int, dtype=COMPUTE_DTYPE, device=None,
 
 def project_qkv(x: SequenceTensor, seed: int = PROJECTION_SEED):
     """x @ Wq, x @ Wk, x @ Wv (attention.py:30-32)."""
-    wq, wk, wv = qkv_projections(x.chan, seed, x.data.device, x.data.dtype)
-    return x.with_data(x.data @ wq), x.with_data(x.data @ wk), x.with_data(x.data @ wv)
+    wq, wk, wv = qkv_projections(x.chan, seed, x.tensor.device, x.tensor.dtype)
+    return x.with_data(x.tensor @ wq), x.with_data(x.tensor @ wk), x.with_data(x.tensor @ wv)
 
 
 # ----------------------------------------------------------------------------- autograd ops
@@ -229,7 +229,7 @@ def _attention(q, k, v, heads, bits, zero_q, scale):
 
 
 def _as_tensor(x):
-    return x.data if isinstance(x, SequenceTensor) else x
+    return x.tensor if isinstance(x, SequenceTensor) else x
 
 
 def dense_attention(q, k, v, key_valid=None, heads: int = 1, scale: float | None = None):

@@ -19,7 +19,7 @@ def write_ospt(path, x: SequenceTensor) -> None:
     """magic "OSPT", version byte, batch/seq/chan as u32 LE, float64 LE payload."""
     if x.kind != REAL:
         raise ValueError("OSPT files store real-kind tensors")
-    data = x.data.detach().to("cpu", torch.float64).contiguous().numpy()
+    data = x.tensor.detach().to("cpu", torch.float64).contiguous().numpy()
     b, s, c = data.shape
     with open(path, "wb") as f:
         f.write(OSPT_MAGIC)

@@ -67,10 +67,25 @@ class GridShape:
         return s // (self.h * self.w), (s // self.w) % self.h, s % self.w
 
 
+_DATA_MODE = ["torch"]
+
+
+def set_data_mode(mode: str) -> str:
+    """How `SequenceTensor.data` reads: "torch" (the device tensor, the default) or "numpy" (a
+    host float64 / uint8 copy, what the reference's numpy callers expect, e.g. its checks and
+    tests, gridseq.py:79-116).  The package itself always uses `SequenceTensor.tensor`.
+    Returns the previous mode."""
+    if mode not in ("torch", "numpy"):
+        raise ValueError("data mode must be 'torch' or 'numpy'")
+    prev = _DATA_MODE[0]
+    _DATA_MODE[0] = mode
+    return prev
+
+
 class SequenceTensor:
     """(batch, seq, chan) tensor with a scalar kind ("real" or "hif8" codes)."""
 
-    __slots__ = ("data", "kind")
+    __slots__ = ("tensor", "kind")
 
     def __init__(self, data, kind: str = REAL):
         if kind not in (REAL, HIF8):
@@ -87,26 +102,43 @@ class SequenceTensor:
         if data.dim() != 3:
             raise ShapeError(f"SequenceTensor data must be (batch, seq, chan), got shape "
                              f"{tuple(data.shape)}")
-        self.data = data
+        self.tensor = data
         self.kind = kind
 
     @property
+    def data(self):
+        """The (batch, seq, chan) values: the device tensor, or in numpy data mode a read-only
+        host copy (float64 for real values, uint8 for HiF8 codes) as the reference returns."""
+        if _DATA_MODE[0] == "numpy":
+            return self.numpy()
+        return self.tensor
+
+    @property
     def batch(self) -> int:
-        return self.data.shape[0]
+        return self.tensor.shape[0]
 
     @property
     def seq(self) -> int:
-        return self.data.shape[1]
+        return self.tensor.shape[1]
 
     @property
     def chan(self) -> int:
-        return self.data.shape[2]
+        return self.tensor.shape[2]
 
     def with_data(self, data) -> "SequenceTensor":
         return SequenceTensor(data, kind=self.kind)
 
     def numpy(self) -> np.ndarray:
-        return self.data.detach().cpu().numpy()
+        t = self.tensor.detach()
+        if self.kind == REAL and t.dtype != torch.float64:
+            t = t.to(torch.float64)
+        a = t.cpu().numpy()
+        a.flags.writeable = False
+        return a
+
+    def __array__(self, dtype=None, copy=None):
+        a = self.numpy()
+        return a.astype(dtype) if dtype is not None else a
 
     @staticmethod
     def zeros(batch: int, seq: int, chan: int, kind: str = REAL, dtype=None,
@@ -234,7 +266,7 @@ class IndexMap:
     def apply(self, x):
         """Gather x through the map; channel vectors are copied verbatim.
         Accepts a SequenceTensor (returns one) or a (batch, seq, chan) tensor."""
-        data = x.data if isinstance(x, SequenceTensor) else x
+        data = x.tensor if isinstance(x, SequenceTensor) else x
         if (data.shape[0], data.shape[1]) != (self.in_batch, self.in_seq):
             raise ShapeError(f"map expects input ({self.in_batch}, {self.in_seq}), got "
                              f"({data.shape[0]}, {data.shape[1]})")

@@ -102,7 +102,7 @@ class ProcessGroup:
     log: CommLog
 
     def __post_init__(self) -> None:
-        shapes = {tuple(s.tensor.data.shape) for s in self.shards}
+        shapes = {tuple(s.tensor.tensor.shape) for s in self.shards}
         if len(shapes) > 1:
             raise ShardingError(f"ranks hold unequal shapes: {sorted(shapes)}")
 
@@ -112,7 +112,7 @@ class ProcessGroup:
 
     @property
     def local_elements(self) -> int:
-        return self.shards[0].tensor.data.numel()
+        return self.shards[0].tensor.tensor.numel()
 
 
 def shard_pattern_layout(x_pattern, group_size: int, log: CommLog | None = None) -> ProcessGroup:
@@ -122,14 +122,14 @@ def shard_pattern_layout(x_pattern, group_size: int, log: CommLog | None = None)
     if xs.batch % group_size:
         raise ShardingError(f"batch {xs.batch} not divisible by group size {group_size}")
     per = xs.batch // group_size
-    shards = tuple(RankShard(r, xs.with_data(xs.data[r * per:(r + 1) * per]))
+    shards = tuple(RankShard(r, xs.with_data(xs.tensor[r * per:(r + 1) * per]))
                    for r in range(group_size))
     return ProcessGroup(shards, log if log is not None else CommLog())
 
 
 def gather_shards(group: ProcessGroup) -> SequenceTensor:
     """Concatenate shards along the batch axis; verification helper (ssp.py:109-113)."""
-    return SequenceTensor(torch.cat([s.tensor.data for s in group.shards], dim=0),
+    return SequenceTensor(torch.cat([s.tensor.tensor for s in group.shards], dim=0),
                           kind=group.shards[0].tensor.kind)
 
 
@@ -170,7 +170,7 @@ def ssp_pattern_switch(group: ProcessGroup, g: GridShape) -> ProcessGroup:
     n = group.size
     first = group.shards[0].tensor
     check_switch(n, first.batch, first.seq, g)
-    send = [kernels.ssp_pack(s.tensor.data, n, g.t, g.h, g.w, g.k) for s in group.shards]
+    send = [kernels.ssp_pack(s.tensor.tensor, n, g.t, g.h, g.w, g.k) for s in group.shards]
     recv = all_to_all(send, group.log, label="pattern-switch")
     out = tuple(RankShard(r, SequenceTensor(
         kernels.ssp_unpack(buf, n, first.batch, g.t, g.h, g.w, g.k), kind=group.shards[r].tensor.kind))
