@@ -260,6 +260,18 @@ int osp_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, int
                     float eps, float* sumsq, const float* rope_table, int64_t t, int64_t h,
                     int64_t w, int64_t k, int pattern, int64_t batch, int64_t row_offset,
                     void* stream);
+/*
+ * Backward of osp_qkv_project's q/k epilogue, IN PLACE on g (rows x >= 2*chan bf16, the gradient
+ * of the normalised + rotated q | k): transpose of the RoPE rotation, then (norm 1 / 2) the
+ * RMSNorm backward r*gamma*g - y*r^3*mean(gamma*g*y) per head / per row, y being the pre-norm
+ * GEMM output (rows x >= 2*chan bf16; may be NULL with norm 0).  Same grid / pattern / row_offset
+ * arguments as the forward.  No reference counterpart (SURVEY.md sec. 8f row 2 is beyond
+ * attention.py:20-32).
+ */
+int osp_qk_norm_rope_bwd(void* g, int64_t g_stride, const void* y, int64_t y_stride, int64_t rows,
+                         int64_t chan, int norm, const float* gamma_q, const float* gamma_k, float eps,
+                         const float* rope_table, int64_t t, int64_t h, int64_t w, int64_t k,
+                         int pattern, int64_t batch, int64_t row_offset, void* stream);
 
 /*
  * K7: the SSP pattern switch as one pull over peer memory (replaces pack -> all_to_all -> unpack,

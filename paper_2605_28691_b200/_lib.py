@@ -58,6 +58,8 @@ _SIGS = {
                        c_int),
     "osp_qkv_project": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_vp, c_f, c_vp, c_vp,
                          c_i64, c_i64, c_i64, c_i64, c_int, c_i64, c_i64, c_vp], c_int),
+    "osp_qk_norm_rope_bwd": ([c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_int, c_vp, c_vp, c_f, c_vp,
+                              c_i64, c_i64, c_i64, c_i64, c_int, c_i64, c_i64, c_vp], c_int),
     "osp_absmax": ([c_vp, c_int, c_i64, c_vp, c_vp], c_int),
     "osp_hif8_scale": ([c_vp, c_i64, ctypes.c_double, ctypes.c_double, c_vp, c_vp], c_int),
     "osp_hif8_encode": ([c_vp, c_int, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp], c_int),

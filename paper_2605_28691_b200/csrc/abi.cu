@@ -577,6 +577,18 @@ int osp_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, int
                             rope_table, t, h, w, k, pattern, batch, row_offset, as_stream(stream));
 }
 
+int osp_qk_norm_rope_bwd(void* g, int64_t g_stride, const void* y, int64_t y_stride, int64_t rows,
+                         int64_t chan, int norm, const float* gamma_q, const float* gamma_k, float eps,
+                         const float* rope_table, int64_t t, int64_t h, int64_t w, int64_t k,
+                         int pattern, int64_t batch, int64_t row_offset, void* stream) {
+  if (rows < 0 || chan <= 0 || !g) {
+    set_error("qk norm/rope backward: bad sizes or null pointers");
+    return kValue;
+  }
+  return launch_qk_norm_rope_bwd(g, g_stride, y, y_stride, rows, chan, norm, gamma_q, gamma_k, eps,
+                                 rope_table, t, h, w, k, pattern, batch, row_offset, as_stream(stream));
+}
+
 int osp_debug_counters(uint64_t* host_out, int n, int reset) {
   return debug_counters(reinterpret_cast<unsigned long long*>(host_out), n, reset);
 }

@@ -93,6 +93,10 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
                        float eps, float* sumsq, const float* rope_table, int64_t t, int64_t h,
                        int64_t w, int64_t k, int pattern, int64_t batch, int64_t row_offset,
                        cudaStream_t stream);
+int launch_qk_norm_rope_bwd(void* g, int64_t g_stride, const void* y, int64_t y_stride, int64_t rows,
+                            int64_t chan, int norm, const float* gamma_q, const float* gamma_k, float eps,
+                            const float* rope_table, int64_t t, int64_t h, int64_t w, int64_t k, int pattern,
+                            int64_t batch, int64_t row_offset, cudaStream_t stream);
 
 int launch_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,
                      int d, cudaStream_t stream);

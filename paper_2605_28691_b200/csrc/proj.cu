@@ -360,6 +360,82 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(ProjArgs a) {
   }
 }
 
+
+// Backward of the q/k epilogue: g, the gradient of the normalised and
+// rotated q | k, becomes the gradient of the pre-norm GEMM output, IN PLACE.  One warp per
+// (row, q|k): transpose of the RoPE pair rotation, dg = gamma * g (with a norm), then the RMSNorm
+// backward dy = r*dg - y*r^3*mean(dg*y) over the head (norm 1) or the whole row (norm 2), with
+// y the pre-norm output and r = rsqrt(mean(y^2) + eps).  fp32 math, bf16 in and out.
+__global__ void __launch_bounds__(256) qk_norm_rope_bwd_kernel(ProjArgs a, __nv_bfloat16* g, int64_t g_stride,
+                                                               const __nv_bfloat16* y, int64_t y_stride) {
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= static_cast<int64_t>(a.rows) * 2) return;
+  const int row = static_cast<int>(gw >> 1);
+  const int which = static_cast<int>(gw & 1);
+  const float* gamma = which == 0 ? a.gamma_q : a.gamma_k;
+  int t = 0, h = 0, w = 0;
+  if (a.rope) row_coords(a, row, t, h, w);
+  __nv_bfloat162* gp = reinterpret_cast<__nv_bfloat162*>(g + static_cast<int64_t>(row) * g_stride +
+                                                         static_cast<int64_t>(which) * a.chan);
+  const __nv_bfloat162* yp = y ? reinterpret_cast<const __nv_bfloat162*>(
+                                     y + static_cast<int64_t>(row) * y_stride + static_cast<int64_t>(which) * a.chan)
+                               : nullptr;
+  // unrotated (and gamma-scaled) gradient of pair pidx
+  auto dg_pair = [&](int pidx) {
+    float2 d = __bfloat1622float2(gp[pidx]);
+    if (a.rope) {
+      const int i = pidx & 63;
+      const float2 cs = i < a.d_t ? a.rope[static_cast<int64_t>(t) * 32 + i]
+                                  : (i < a.d_t + a.d_h ? a.rope[static_cast<int64_t>(a.T + h) * 32 + (i - a.d_t)]
+                                                       : a.rope[static_cast<int64_t>(a.T + a.H + w) * 32 +
+                                                                (i - a.d_t - a.d_h)]);
+      d = make_float2(d.x * cs.x + d.y * cs.y, -d.x * cs.y + d.y * cs.x);
+    }
+    if (a.norm && gamma) {
+      const int c = 2 * pidx;
+      d.x *= __ldg(gamma + c);
+      d.y *= __ldg(gamma + c + 1);
+    }
+    return d;
+  };
+  auto warp_sum = [](float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+  };
+  const int n_pairs = a.chan / 2;
+  if (a.norm == 0) {
+    for (int pidx = lane; pidx < n_pairs; pidx += 32) {
+      const float2 d = dg_pair(pidx);
+      gp[pidx] = __floats2bfloat162_rn(d.x, d.y);
+    }
+    return;
+  }
+  // norm 1: groups of 64 pairs (one head), lanes take pairs lane and lane + 32 of the group;
+  // norm 2: one group spanning the row
+  const int group_pairs = a.norm == 1 ? 64 : n_pairs;
+  for (int p0 = 0; p0 < n_pairs; p0 += group_pairs) {
+    float ss = 0.f, sd = 0.f;
+    for (int pidx = p0 + lane; pidx < p0 + group_pairs; pidx += 32) {
+      const float2 d = dg_pair(pidx);
+      const float2 v = __bfloat1622float2(yp[pidx]);
+      ss = fmaf(v.x, v.x, fmaf(v.y, v.y, ss));
+      sd = fmaf(d.x, v.x, fmaf(d.y, v.y, sd));
+    }
+    ss = warp_sum(ss);
+    sd = warp_sum(sd);
+    const float n = 2.f * group_pairs;
+    const float r = rsqrtf(ss / n + a.eps);
+    const float coef = r * r * r * (sd / n);
+    for (int pidx = p0 + lane; pidx < p0 + group_pairs; pidx += 32) {
+      const float2 d = dg_pair(pidx);
+      const float2 v = __bfloat1622float2(yp[pidx]);
+      gp[pidx] = __floats2bfloat162_rn(r * d.x - v.x * coef, r * d.y - v.y * coef);
+    }
+  }
+}
+
 }  // namespace
 
 int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, int64_t chan,
@@ -460,6 +536,54 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   const int64_t warps = rows * 2;
   qk_norm_rope_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, stream>>>(a);
   return check_cuda(cudaGetLastError(), "qk_norm_rope launch");
+}
+
+int launch_qk_norm_rope_bwd(void* g, int64_t g_stride, const void* y, int64_t y_stride, int64_t rows,
+                            int64_t chan, int norm, const float* gamma_q, const float* gamma_k, float eps,
+                            const float* rope_table, int64_t t, int64_t h, int64_t w, int64_t k, int pattern,
+                            int64_t batch, int64_t row_offset, cudaStream_t stream) {
+  if (chan % 128 != 0 || chan < 128) {
+    set_error("qk norm/rope backward: chan must be a positive multiple of 128 (head_dim 128)");
+    return kUnsupported;
+  }
+  if (norm < 0 || norm > 2 || (norm != 0 && !y)) {
+    set_error("qk norm/rope backward: norm must be 0, 1 or 2 (1 and 2 need the pre-norm output y)");
+    return kValue;
+  }
+  if (g_stride < 2 * chan || (norm && y_stride < 2 * chan) || (g_stride * 2) % 4 || (y_stride * 2) % 4) {
+    set_error("qk norm/rope backward: row strides must cover q|k and keep bf16 pairs aligned");
+    return kValue;
+  }
+  if (rows == 0) return kOk;
+  ProjArgs a{};
+  a.rows = static_cast<int>(rows);
+  a.chan = static_cast<int>(chan);
+  a.norm = norm;
+  a.gamma_q = gamma_q;
+  a.gamma_k = gamma_k;
+  a.eps = eps;
+  a.rope = reinterpret_cast<const float2*>(rope_table);
+  a.pattern = pattern;
+  a.B = static_cast<int>(batch);
+  a.T = static_cast<int>(t);
+  a.H = static_cast<int>(h);
+  a.W = static_cast<int>(w);
+  a.k = static_cast<int>(k);
+  a.row_offset = static_cast<int>(row_offset);
+  const int64_t k2 = k * k;
+  a.L = pattern == 0 ? static_cast<int>(t * h * w) : static_cast<int>(t * h * w / k2);
+  a.d_t = (128 - 4 * (128 / 6)) / 2;
+  a.d_h = (2 * (128 / 6)) / 2;
+  if (rope_table && (pattern < 0 || pattern > 2 || k < 1 || (pattern == 1 && (h % k || w % k)) ||
+                     (pattern == 2 && (h % k2 || w % k2)) || row_offset < 0 ||
+                     rows + row_offset > batch * t * h * w)) {
+    set_error("qk norm/rope backward: rope needs a pattern layout consistent with the grid");
+    return kPattern;
+  }
+  const int64_t warps = rows * 2;
+  qk_norm_rope_bwd_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, stream>>>(
+      a, static_cast<__nv_bfloat16*>(g), g_stride, static_cast<const __nv_bfloat16*>(y), y_stride);
+  return check_cuda(cudaGetLastError(), "qk_norm_rope_bwd launch");
 }
 
 }  // namespace osp

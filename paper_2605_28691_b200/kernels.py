@@ -531,6 +531,25 @@ def hif8_decode(codes: torch.Tensor, table: torch.Tensor, dtype=torch.float64,
     return out
 
 
+def qk_norm_rope_bwd(g: torch.Tensor, y: torch.Tensor | None, norm: int, gamma_q, gamma_k, eps: float,
+                     rope_tab, grid, pattern: int, batch: int, row_offset: int = 0) -> torch.Tensor:
+    """Backward of K6's q/k epilogue, in place on g (rows, >= 2C) bf16: transpose RoPE rotation,
+    then the RMSNorm backward against the pre-norm output y (rows, >= 2C) bf16."""
+    L = _lib.lib()
+    _cuda(g, "g")
+    if g.dtype != torch.bfloat16 or (y is not None and y.dtype != torch.bfloat16):
+        raise UnsupportedError("qk_norm_rope_bwd runs bf16 g and y")
+    rows, W3 = g.shape
+    C = W3 // 3
+    gq = None if gamma_q is None else gamma_q.to(device=g.device, dtype=torch.float32).contiguous()
+    gk = None if gamma_k is None else gamma_k.to(device=g.device, dtype=torch.float32).contiguous()
+    _lib.check(STATS.run("qk_norm_rope_bwd", 1, lambda: L.osp_qk_norm_rope_bwd(
+        g.data_ptr(), g.stride(0), _lib.ptr(y), y.stride(0) if y is not None else 0, rows, C, norm,
+        _lib.ptr(gq), _lib.ptr(gk), float(eps), _lib.ptr(rope_tab), grid.t, grid.h, grid.w, grid.k,
+        pattern, batch, row_offset, _lib.stream_ptr(g.device))))
+    return g
+
+
 def qkv_project(x: torch.Tensor, w_t: torch.Tensor, norm: int, gamma_q, gamma_k, eps: float,
                 rope_tab, grid, pattern: int, batch: int, row_offset: int = 0) -> torch.Tensor:
     """K6: (rows, C) bf16 @ w_t^T (w_t (3C, C) bf16) with the q/k norm + RoPE epilogue."""

@@ -84,27 +84,10 @@ def qkv_project(x: torch.Tensor, grid: GridShape, pattern: SparsePattern = Spars
     return out.view(*shape[:-1], 3 * C)
 
 
-def _rope_cos_sin(grid: GridShape, pattern, batch: int, rows: int, row_offset: int, device, theta):
-    """(rows, 64) cos / sin of every pair's angle (backward only)."""
-    pat = SparsePattern(pattern)
-    if pat is SparsePattern.ORIGINAL:
-        flat = torch.arange(grid.seq_len, device=device)
-        src = flat.repeat(batch)
-    else:
-        from .skiparse import pattern_map
-        src = pattern_map(grid, pat, batch).src.reshape(-1) % grid.seq_len
-    src = src[row_offset:row_offset + rows]
-    t, h, w = src // (grid.h * grid.w), (src // grid.w) % grid.h, src % grid.w
-    tab = rope_table(grid, 128, theta, device)                      # (t+h+w, 32, 2)
-    dt, dh, dw = (d // 2 for d in rope_axes(128))
-    cs = torch.cat([tab[t, :dt], tab[grid.t + h, :dh], tab[grid.t + grid.h + w, :dw]], dim=1)
-    return cs[..., 0], cs[..., 1]
-
-
 class QKVPrologue(torch.autograd.Function):
-    """K6 forward; backward = inverse RoPE rotation, RMSNorm backward (fp32 torch on the
-    device), then dx = d(pre-norm qkv) @ W^T.  Weights and gammas are fixed (no grad), like the
-    reference's seeded projections."""
+    """K6 forward; backward = one K6b kernel (inverse RoPE rotation + RMSNorm backward, in place
+    on the bf16 gradient, fp32 math), then dx = d(pre-norm qkv) @ W^T.  Weights and gammas are
+    fixed (no grad), like the reference's seeded projections."""
 
     @staticmethod
     def forward(ctx, x, grid, pattern, batch, norm, gamma_q, gamma_k, eps, rope, row_offset,
@@ -123,28 +106,14 @@ class QKVPrologue(torch.autograd.Function):
         grid, pattern, batch, norm, gamma_q, gamma_k, eps, rope, row_offset, C, w_t = ctx.cfg
         shape = x.shape
         rows = x.numel() // C
-        g = gout.reshape(rows, 3 * C).float()
+        g = gout.reshape(rows, 3 * C).to(torch.bfloat16)
         if norm is not None or rope:
-            y = qkv_project(x, grid, pattern, batch, weight_t=w_t).reshape(rows, 3 * C).float() if norm else None
-            if rope:
-                c, s = _rope_cos_sin(grid, pattern, batch, rows, row_offset, x.device, ROPE_THETA)
-            parts = []
-            for which, gamma in ((0, gamma_q), (1, gamma_k)):
-                d = g[:, which * C:(which + 1) * C]
-                if rope:   # transpose of the pair rotation
-                    d2 = d.view(rows, -1, 64, 2)
-                    d0, d1 = d2[..., 0], d2[..., 1]
-                    d = torch.stack([d0 * c[:, None] + d1 * s[:, None],
-                                     -d0 * s[:, None] + d1 * c[:, None]], dim=-1).reshape(rows, C)
-                if norm is not None:
-                    yy = y[:, which * C:(which + 1) * C]
-                    n = C if norm == "channel" else 128
-                    yg = yy.view(rows, -1, n)
-                    dg = (d * (gamma.float() if gamma is not None else 1.0)).view(rows, -1, n)
-                    r = torch.rsqrt((yg * yg).mean(-1, keepdim=True) + eps)
-                    d = (r * dg - yg * (r ** 3) * (dg * yg).mean(-1, keepdim=True)).reshape(rows, C)
-                parts.append(d)
-            parts.append(g[:, 2 * C:])
-            g = torch.cat(parts, dim=1)
-        dx = (g.to(torch.bfloat16) @ w_t).reshape(shape)
+            # K6b, in place on a private copy of the incoming gradient: transpose RoPE rotation and
+            # the RMSNorm backward against the recomputed pre-norm output
+            g = g.clone() if g.data_ptr() == gout.data_ptr() else g.contiguous()
+            y = qkv_project(x, grid, pattern, batch, weight_t=w_t).reshape(rows, 3 * C) if norm else None
+            kernels.qk_norm_rope_bwd(g, y, _NORMS[norm], gamma_q, gamma_k, eps,
+                                     rope_table(grid, 128, ROPE_THETA, x.device) if rope else None,
+                                     grid, _PATTERN_IDS[SparsePattern(pattern)], batch, row_offset)
+        dx = (g @ w_t).reshape(shape)
         return dx, None, None, None, None, None, None, None, None, None, None

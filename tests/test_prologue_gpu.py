@@ -80,10 +80,11 @@ def test_prologue_errors(P):
         qkv_project(torch.zeros(64, 128, device="cuda", dtype=torch.bfloat16), g, norm="layer")
 
 
-@pytest.mark.parametrize("norm,rope", [(None, True), ("head", True), ("channel", True), ("head", False)])
-def test_prologue_backward_matches_float64_autograd(P, norm, rope):
-    """QKVPrologue backward (inverse RoPE, RMSNorm backward, dx = dqkv W^T) vs float64 autograd
-    of the reference prologue."""
+@pytest.mark.parametrize("norm,rope,pat", [(None, True, "tsa"), ("head", True, "tsa"), ("channel", True, "tsa"),
+                                          ("head", False, "tsa"), ("head", True, "gsa"), ("channel", True, "gsa")])
+def test_prologue_backward_matches_float64_autograd(P, norm, rope, pat):
+    """QKVPrologue backward (K6b: inverse RoPE + RMSNorm backward; dx = dqkv W^T) vs float64
+    autograd of the reference prologue."""
     from paper_2605_28691_b200.prologue import QKVPrologue, packed_projection_t
     g = P.GridShape(2, 8, 8, 2)
     og = O.Grid(2, 8, 8, 2)
@@ -93,11 +94,12 @@ def test_prologue_backward_matches_float64_autograd(P, norm, rope):
     gq = torch.rand(C, device="cuda") + 0.5
     gk = torch.rand(C, device="cuda") + 0.5
     w_t = packed_projection_t(C, "cuda")
-    y = QKVPrologue.apply(x, g, P.SparsePattern.TOKEN_WISE, 1, norm, gq, gk, 1e-6, rope, 0, w_t)
+    sp = P.SparsePattern.TOKEN_WISE if pat == "tsa" else P.SparsePattern.GROUP_WISE
+    y = QKVPrologue.apply(x, g, sp, 1, norm, gq, gk, 1e-6, rope, 0, w_t)
     gy = torch.randn_like(y)
     y.backward(gy)
     xr = x.detach().double().cpu().reshape(-1, C).requires_grad_(True)
-    pos = R.pattern_positions(og, "tsa", 1)
+    pos = R.pattern_positions(og, pat, 1)
     ref = R.qkv_prologue_ref(xr, w_t.t().double().cpu(), pos, norm, gq.cpu(), gk.cpu(), rope=rope)
     ref.backward(gy.double().cpu().reshape(-1, 3 * C))
     got = x.grad.double().cpu().reshape(-1, C)
