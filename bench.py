@@ -421,8 +421,30 @@ def run_ours(args, world, rank, local_rank):
     torch.cuda.synchronize()
     barrier()
 
+    # ---- CUDA graph of the whole step (fwd + bwd), replayed in the timed region when the step is
+    # launch-bound (--graph; "auto" = the cfg1 reference case): the kernels take device pointers,
+    # sizes and the current stream only, so the step captures as is.  Per-kernel times then come
+    # from one extra eager pass after the timed region.
+    use_graph = (args.graph == "on") or (args.graph == "auto" and args.config == "cfg1" and world == 1)
+    graph = None
+    if use_graph:
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                x.grad = None
+                step(x)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        x.grad = None
+        with torch.cuda.graph(graph):
+            step(x)
+        graph.replay()
+        torch.cuda.synchronize()
+
     # ---- device-resident timed region
-    kernels.STATS.reset(timing=True)
+    kernels.STATS.reset(timing=graph is None)
     log.events.clear()
     log.timed.clear()
     log.timing = world > 1
@@ -435,12 +457,22 @@ def run_ours(args, world, rank, local_rank):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            x.grad = None
-            step(x)
+            if graph is not None:
+                graph.replay()
+            else:
+                x.grad = None
+                step(x)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
     ms = e0.elapsed_time(e1)
+    if graph is not None:
+        # the launches and kernel times of the replayed steps, from an eager pass of the same step
+        kernels.STATS.reset(timing=True)
+        for _ in range(args.steps):
+            x.grad = None
+            step(x)
+        torch.cuda.synchronize()
     launches = kernels.STATS.launches
     per_kernel = kernels.STATS.elapsed_ms()
     comm = _comm_summary(log, args.steps) if world > 1 else None   # the timed steps only
@@ -587,7 +619,11 @@ def run_ours(args, world, rank, local_rank):
                        "parallelism": (f"ssp{ssp_n}" + (f"xulysses{uly_n}" if uly_n > 1 else "")
                                        + (f"xdp{dp}" if dp > 1 else "")),
                        "padded_grid": [blk.grid.t, blk.grid.h, blk.grid.w], "subseq_len": blk.L,
-                       "l2": "inputs > 126 MB L2 (no flush needed)",
+                       "l2": ("inputs > 126 MB L2 (no flush needed)" if T * H * W * C * 2 > 126e6 else
+                              "input x < L2, but each step's q|k|v, O and dO (> L2) evict it: no flush"
+                              if T * H * W * 3 * C * 2 > 126e6 else
+                              "whole step < L2: the launch-bound reference case, no flush"),
+                       "cuda_graph": graph is not None,
                        "block": step_desc},
             "e2e": {"value": e2e_value, "unit": "tokens/s",
                     "h2d_bytes_per_step": io_bytes,
@@ -630,6 +666,8 @@ def main():
     ap.add_argument("--no-comparator", action="store_true", help="skip the same-box SDPA timings")
     ap.add_argument("--tsa-step", action="store_true",
                     help="N=1: time the token-wise steady-state block instead of the orig->orig step")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the step as one CUDA graph in the timed region (auto: cfg1 only)")
     ap.add_argument("--transport", default="auto", choices=["auto", "native", "hif8", "p2p"],
                     help="SSP switch transport for N > 1 (auto = native NCCL; p2p = K7 peer pull, one host)")
     args = ap.parse_args()
