@@ -21,8 +21,9 @@
 // CTA; each CTA's TMA lands its operands in its own smem and completes on the leader's barrier;
 // 6-stage ring of 32 KB per CTA.  Alternative (OSP_PROJ_PAIR=0): two independent M=128 CTAs with
 // the weight slice TMA-multicast into both, 4 stages of 48 KB.  Either way, two 256-column TMEM
-// accumulators let the epilogue of tile i overlap the main loop of tile i+1, and tile pairs are
-// visited in bands (OSP_PROJ_BAND pairs, default 12) across all column tiles.
+// accumulators let the epilogue of tile i overlap the main loop of tile i+1, and tiles are visited
+// in bands of OSP_PROJ_BAND (default 12) column tiles swept over all row pairs (OSP_PROJ_ORDER=0:
+// bands of row pairs swept over all column tiles).
 #include "osp_common.cuh"
 #include "osp_internal.h"
 
@@ -56,6 +57,7 @@ struct ProjArgs {
   int64_t out_stride;
   int rows, chan, n_cols, n_pairs_m, n_tiles_n, k_steps;
   int band;                 // rasterisation: tile pairs per band (all column tiles per band)
+  int col_bands;            // 1: bands of `band` column tiles over all row pairs instead
   int norm;                 // 0 none, 1 per head, 2 per token (two-phase)
   const float* gamma_q;     // (C) or null
   const float* gamma_k;
@@ -157,6 +159,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
   const int n_units = a.n_pairs_m * a.n_tiles_n;  // a unit = two vertically adjacent tiles
   auto tile_mn = [&](int id, int& tm, int& tn) {
+    if (a.col_bands) {  // bands of a.band column tiles swept over all row pairs (W band L2-resident)
+      const int band_units = a.band * a.n_pairs_m;
+      const int band = id / band_units;
+      const int rem = id % band_units;
+      const int cols_in_band = min(a.band, a.n_tiles_n - band * a.band);
+      tn = band * a.band + rem % cols_in_band;
+      tm = 2 * (rem / cols_in_band) + static_cast<int>(crank);
+      return;
+    }
     const int band_units = a.band * a.n_tiles_n;
     const int band = id / band_units;
     const int rem = id % band_units;
@@ -506,6 +517,10 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
     const char* be = getenv("OSP_PROJ_BAND");
     a.band = be ? atoi(be) : 12;  // measured best at cfg3 (tools/bench_proj.py, OSP_PROJ_BAND)
     if (a.band < 1) a.band = 12;
+    // column bands (the band's W slice stays L2-resident while x streams): at cfg3 8.9 GB of DRAM
+    // reads per launch instead of 13.5 with row bands, 2-3% faster (profiles/r02_proj_order.txt)
+    const char* oe = getenv("OSP_PROJ_ORDER");
+    a.col_bands = oe ? atoi(oe) : 1;
   }
   const char* pe = getenv("OSP_PROJ_PAIR");
   const bool pair = pe ? atoi(pe) != 0 : true;
