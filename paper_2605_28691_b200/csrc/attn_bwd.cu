@@ -1121,10 +1121,8 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
   a.scale_log2 = scale * kLog2e;
   a.k_rows = static_cast<const __nv_bfloat16*>(k);
   a.k_row_stride = ks;
-  {
-    const char* f = getenv("OSP_BWD_FLAGS");
-    a.flags = f ? atoi(f) : 0;
-  }
+  static const int bwd_flags = env_int("OSP_BWD_FLAGS", 0);
+  a.flags = bwd_flags;
   static std::atomic<uint64_t> attr_done_v1{0}, attr_done_v2{0};
   if constexpr (D == 128)
     rc = set_smem_attr(reinterpret_cast<const void*>(attn_bwd_v2_kernel), BwdV2Layout::kSmemX, attr_done_v2,

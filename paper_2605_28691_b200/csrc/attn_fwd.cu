@@ -651,10 +651,8 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
   a.n_zero = static_cast<int>(s.n_zero);
   a.scale_log2 = scale * 1.4426950408889634f;
   a.zero_invalid_q = zero_invalid_q;
-  {
-    const char* fl = getenv("OSP_FWD_FLAGS");
-    a.flags = fl ? atoi(fl) : 0;
-  }
+  static const int fwd_flags = env_int("OSP_FWD_FLAGS", 0);
+  a.flags = fwd_flags;
   const int n_qt = static_cast<int>((s.seq_len + kBM - 1) / kBM);
   dim3 grid((n_qt + 1) / 2, static_cast<unsigned>(s.heads), static_cast<unsigned>(s.n_seq));
   static std::atomic<uint64_t> attr_done{0};

@@ -1,6 +1,8 @@
 // Internal (non-ABI) declarations shared by the .cu translation units.
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -9,6 +11,13 @@
 #include <string>
 
 namespace osp {
+
+// Integer tuning / experiment switch from the environment (read by the callers into function-local
+// statics, i.e. once per process); dflt when unset.
+inline int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
 
 // Thread-local error message backing osp_last_error().
 void set_error(const std::string& msg);

@@ -513,17 +513,14 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   rc = set_smem_attr(reinterpret_cast<const void*>(qkv_gemm_kernel<true>), Proj2Layout::kSmem, attr_done_2,
                      "cudaFuncSetAttribute(qkv_gemm pair)");
   if (rc != kOk) return rc;
-  {
-    const char* be = getenv("OSP_PROJ_BAND");
-    a.band = be ? atoi(be) : 12;  // measured best at cfg3 (tools/bench_proj.py, OSP_PROJ_BAND)
-    if (a.band < 1) a.band = 12;
-    // column bands (the band's W slice stays L2-resident while x streams): at cfg3 8.9 GB of DRAM
-    // reads per launch instead of 13.5 with row bands, 2-3% faster (profiles/r02_proj_order.txt)
-    const char* oe = getenv("OSP_PROJ_ORDER");
-    a.col_bands = oe ? atoi(oe) : 1;
-  }
-  const char* pe = getenv("OSP_PROJ_PAIR");
-  const bool pair = pe ? atoi(pe) != 0 : true;
+  // bands of 12 (measured best at cfg3, tools/bench_proj.py); column bands (the band's W slice
+  // stays L2-resident while x streams): at cfg3 8.9 GB of DRAM reads per launch instead of 13.5
+  // with row bands, 2-3% faster (profiles/r02_proj_order.txt)
+  static const int band = env_int("OSP_PROJ_BAND", 12);
+  static const int col_bands = env_int("OSP_PROJ_ORDER", 1);
+  static const bool pair = env_int("OSP_PROJ_PAIR", 1) != 0;
+  a.band = band < 1 ? 12 : band;
+  a.col_bands = col_bands;
   if (norm == 2) {
     rc = check_cuda(cudaMemsetAsync(sumsq, 0, rows * 2 * sizeof(float), stream), "memset sumsq");
     if (rc != kOk) return rc;
