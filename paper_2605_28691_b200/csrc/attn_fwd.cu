@@ -61,6 +61,13 @@ constexpr int kPolyChunks = OSP_FWD_POLY_CHUNKS;
 #define OSP_FWD_PINGPONG 0
 #endif
 
+// V tiles get a deeper ring than K: V_j is released only by PV_{j} of the second query tile, late
+// in the key loop, so with two stages its reload has about one key tile of lead
+#ifndef OSP_FWD_VSTAGES
+#define OSP_FWD_VSTAGES 2
+#endif
+constexpr int kFwdVStages = OSP_FWD_VSTAGES;
+
 template <int D>
 struct FwdLayout {
   static constexpr int kSub = D / 64;
@@ -68,7 +75,7 @@ struct FwdLayout {
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + 2 * kTile;
   static constexpr int kV = kK + 2 * kTile;
-  static constexpr int kBar = kV + 2 * kTile;
+  static constexpr int kBar = kV + kFwdVStages * kTile;
   static constexpr int kSmem = kBar + 256 + 1024;
 };
 
@@ -122,13 +129,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* bar_q = bars + 0;
   uint64_t* bar_kf = bars + 2;
   uint64_t* bar_ke = bars + 4;
-  uint64_t* bar_vf = bars + 6;
-  uint64_t* bar_ve = bars + 8;
-  uint64_t* bar_s = bars + 10;
-  uint64_t* bar_p = bars + 12;
-  uint64_t* bar_o = bars + 14;
-  uint64_t* bar_pb = bars + 16;  // second P half (OSP_FWD_SPLITPV)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* bar_s = bars + 6;
+  uint64_t* bar_p = bars + 8;
+  uint64_t* bar_o = bars + 10;
+  uint64_t* bar_pb = bars + 12;  // second P half (OSP_FWD_SPLITPV)
+  uint64_t* bar_vf = bars + 14;  // [kFwdVStages]
+  uint64_t* bar_ve = bars + 14 + kFwdVStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14 + 2 * kFwdVStages);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -168,12 +175,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(bar_q + i, 1);
       mbar_init(bar_kf + i, 1);
       mbar_init(bar_ke + i, 1);
-      mbar_init(bar_vf + i, 1);
-      mbar_init(bar_ve + i, 1);
+
       mbar_init(bar_s + i, 1);
       mbar_init(bar_p + i, 128);
       mbar_init(bar_pb + i, 128);
       mbar_init(bar_o + i, 1);
+    }
+    for (int i = 0; i < kFwdVStages; ++i) {
+      mbar_init(bar_vf + i, 1);
+      mbar_init(bar_ve + i, 1);
     }
     fence_barrier_init();
   }
@@ -217,10 +227,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (lane == 0) mbar_expect_tx(bar_kf + st, Ly::kTile);
       __syncwarp();
       gather_tile(sm + Ly::kK + st * Ly::kTile, &tmK, bar_kf + st, j * kBN);
-      mbar_wait(bar_ve + st, ph ^ 1);
-      if (lane == 0) mbar_expect_tx(bar_vf + st, Ly::kTile);
+      const int vs = j % kFwdVStages;
+      mbar_wait(bar_ve + vs, ((j / kFwdVStages) & 1) ^ 1);
+      if (lane == 0) mbar_expect_tx(bar_vf + vs, Ly::kTile);
       __syncwarp();
-      gather_tile(sm + Ly::kV + st * Ly::kTile, &tmV, bar_vf + st, j * kBN);
+      gather_tile(sm + Ly::kV + vs * Ly::kTile, &tmV, bar_vf + vs, j * kBN);
     }
   } else if (warp == 0) {
     if (elect_one()) {
@@ -241,8 +252,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if ((flags & 8) && j >= 2) {  // experiment 8: no K/V reloads (stale tiles, timing only)
           mbar_wait(bar_ke + st, ph ^ 1);
           mbar_arrive(bar_kf + st);
-          mbar_wait(bar_ve + st, ph ^ 1);
-          mbar_arrive(bar_vf + st);
+          mbar_wait(bar_ve + j % kFwdVStages, ((j / kFwdVStages) & 1) ^ 1);
+          mbar_arrive(bar_vf + j % kFwdVStages);
           continue;
         }
         mbar_wait(bar_ke + st, ph ^ 1);
@@ -251,11 +262,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int s = 0; s < Ly::kSub; ++s)
           tma_load_3d(sm + Ly::kK + st * Ly::kTile + s * 16384, &tmK, bar_kf + st,
                       head * D + s * 64, j * kBN, seq);
-        mbar_wait(bar_ve + st, ph ^ 1);
-        mbar_expect_tx(bar_vf + st, Ly::kTile);
+        const int vs = j % kFwdVStages;
+        mbar_wait(bar_ve + vs, ((j / kFwdVStages) & 1) ^ 1);
+        mbar_expect_tx(bar_vf + vs, Ly::kTile);
 #pragma unroll
         for (int s = 0; s < Ly::kSub; ++s)
-          tma_load_3d(sm + Ly::kV + st * Ly::kTile + s * 16384, &tmV, bar_vf + st,
+          tma_load_3d(sm + Ly::kV + vs * Ly::kTile + s * 16384, &tmV, bar_vf + vs,
                       head * D + s * 64, j * kBN, seq);
       }
     }
@@ -341,16 +353,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #if OSP_FWD_TIMING
         m0 = clock64();
 #endif
-        pv(1, (j - 1) & 1, j - 1 > 0, (j - 1) & 1, bar_ve + ((j - 1) & 1), nullptr, nullptr);
+        pv(1, (j - 1) % kFwdVStages, j - 1 > 0, (j - 1) & 1, bar_ve + (j - 1) % kFwdVStages, nullptr, nullptr);
         OSP_MT(1);
       }
       qk(1, st, bar_s + 1, bar_ke + st);
 #if OSP_FWD_TIMING
       m0 = clock64();
 #endif
-      mbar_wait(bar_vf + st, ph);
+      mbar_wait(bar_vf + j % kFwdVStages, (j / kFwdVStages) & 1);
       OSP_MT(2);
-      pv(0, st, j > 0, j & 1, nullptr, nullptr, nullptr);
+      pv(0, j % kFwdVStages, j > 0, j & 1, nullptr, nullptr, nullptr);
       OSP_MT(3);
     }
 #if OSP_FWD_TIMING
@@ -358,7 +370,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     atomicAdd(&g_fwd_counters[20], static_cast<unsigned long long>(n_kv));
 #endif
     const int last = n_kv - 1;
-    pv(1, last & 1, last > 0, last & 1, bar_ve + (last & 1), bar_o + 0, bar_o + 1);
+    pv(1, last % kFwdVStages, last > 0, last & 1, bar_ve + last % kFwdVStages, bar_o + 0, bar_o + 1);
     }
     __syncwarp();
   }
