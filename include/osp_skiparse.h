@@ -304,6 +304,8 @@ int osp_peer_gather(const void* const* srcs, int n_src, int64_t stride_rows, con
 /* Profiling counters of instrumented builds (-DOSP_FWD_TIMING=1): copies n <= 64 uint64 into
  * host_out (zeros in normal builds) and optionally resets them.  Not part of the hot path. */
 int osp_debug_counters(uint64_t* host_out, int n, int reset);
+/* The same for the K3 backward's phase counters (OSP_BWD_TIMING=1 builds). */
+int osp_debug_counters_bwd(uint64_t* host_out, int n, int reset);
 
 /* Self-test of the tcgen05 instruction forms (S = A B^T, O = bf16(S) V for one 128-row tile). */
 int osp_debug_mma(const void* a, const void* b, const void* v, float* s_out, float* o_out,

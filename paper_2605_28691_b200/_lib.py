@@ -72,6 +72,7 @@ _SIGS = {
     "osp_peer_barrier": ([c_vp, c_int, c_int, ctypes.c_uint32, c_i64, c_vp, c_vp], c_int),
     "osp_peer_gather": ([c_vp, c_int, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp], c_int),
     "osp_debug_counters": ([c_vp, c_int, c_int], c_int),
+    "osp_debug_counters_bwd": ([c_vp, c_int, c_int], c_int),
     "osp_debug_mma": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp], c_int),
 }
 

@@ -30,6 +30,7 @@ int launch_hif8_scale(const double* amax, int64_t count, double target, double e
                       cudaStream_t stream);
 
 int debug_counters(unsigned long long* host, int n, int reset);
+int debug_counters_bwd(unsigned long long* host, int n, int reset);
 
 static thread_local std::string g_err;
 
@@ -587,6 +588,10 @@ int osp_qk_norm_rope_bwd(void* g, int64_t g_stride, const void* y, int64_t y_str
   }
   return launch_qk_norm_rope_bwd(g, g_stride, y, y_stride, rows, chan, norm, gamma_q, gamma_k, eps,
                                  rope_table, t, h, w, k, pattern, batch, row_offset, as_stream(stream));
+}
+
+int osp_debug_counters_bwd(uint64_t* host_out, int n, int reset) {
+  return debug_counters_bwd(reinterpret_cast<unsigned long long*>(host_out), n, reset);
 }
 
 int osp_debug_counters(uint64_t* host_out, int n, int reset) {

@@ -29,7 +29,28 @@
 #define OSP_BWD_EXPERIMENTS 0
 #endif
 
+// Phase timing (-DOSP_BWD_TIMING=1 builds only): clock64 sums of the v2 kernel's MMA issuer waits
+// and of the first compute / writer warp's phases, read back with osp_debug_counters_bwd().
+#ifndef OSP_BWD_TIMING
+#define OSP_BWD_TIMING 0
+#endif
+
+// Ring depths of the d = 128 kernel: Q / dO stages and dQ staging buffers (shared memory allows
+// 2 + 2 or 3 + 1)
+#ifndef OSP_BWD_QSTAGES
+#define OSP_BWD_QSTAGES 2
+#endif
+#ifndef OSP_BWD_XBUFS
+#define OSP_BWD_XBUFS 2
+#endif
+// Q (+ lse2 / delta) and dO of a stage complete on separate barriers, so S^T_{i+1} (which needs only
+// Q) is not held back by the dO half of the stage
+#ifndef OSP_BWD_SPLITQ
+#define OSP_BWD_SPLITQ 1
+#endif
+
 namespace osp {
+__device__ unsigned long long g_bwd_counters[64];
 namespace {
 
 constexpr int kBwdThreads = 384;
@@ -439,8 +460,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 struct BwdV2Layout {
   static constexpr int kK = 0;                    // 128 keys x 128 d  (2 x 16 KB)
   static constexpr int kV = 32768;
-  static constexpr int kStages = 2;
-  static constexpr int kQ = 65536;                // 3 x (64 q x 128 d = 2 x 8 KB)
+  static constexpr int kStages = OSP_BWD_QSTAGES;  // Q / dO ring depth
+  static constexpr int kQ = 65536;                // stages x (64 q x 128 d = 2 x 8 KB)
   static constexpr int kDO = kQ + kStages * 16384;
   static constexpr int kDS = kDO + kStages * 16384;   // 2 x (128 keys x 64 q) bf16
   static constexpr int kStat = kDS + 2 * 16384;       // 3 x (lse2[64], delta[64])
@@ -448,7 +469,7 @@ struct BwdV2Layout {
   static constexpr int kSmem = kBar + 256;
   // dQ^T staging for the asynchronous bulk reduction: one 64-query tile in the accumulator's
   // (q/4, d, q%4) layout = 32 KB
-  static constexpr int kXBufs = 2;
+  static constexpr int kXBufs = OSP_BWD_XBUFS;
   static constexpr int kX = kSmem;
   static constexpr int kSmemX = kX + kXBufs * 32768;
 };
@@ -481,7 +502,8 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
   uint64_t* bar_dqf = bars + 16;  // [2] 128 arrivals
   uint64_t* bar_fin = bars + 18;
   uint64_t* bar_kt = bars + 19;   // K rows in TMEM (256 arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint64_t* bar_df = OSP_BWD_SPLITQ ? bars + 21 : bar_qf;  // [3] dO of a stage landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -504,6 +526,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
     mbar_init(bar_kv, 1);
     for (int i = 0; i < Ly::kStages; ++i) {
       mbar_init(bar_qf + i, 1);
+      if (OSP_BWD_SPLITQ) mbar_init(bar_df + i, 1);
       mbar_init(bar_qe + i, 1);
     }
     mbar_init(bar_s, 1);
@@ -567,14 +590,20 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         const int st = i % Ly::kStages;
         mbar_wait(bar_qe + st, ((i / Ly::kStages) & 1) ^ 1);
         if (lane == 0) {
-          mbar_expect_tx(bar_qf + st, 2 * 16384 + 512);
+          if (OSP_BWD_SPLITQ) {
+            mbar_expect_tx(bar_qf + st, 16384 + 512);
+            mbar_expect_tx(bar_df + st, 16384);
+          } else {
+            mbar_expect_tx(bar_qf + st, 2 * 16384 + 512);
+          }
           bulk_load(sm + Ly::kStat + st * 512, lse2_g + i * 64, 256, bar_qf + st);
           bulk_load(sm + Ly::kStat + st * 512 + 256, delta_g + i * 64, 256, bar_qf + st);
         }
         __syncwarp();
         const int4 r = rows4(i * 64 + 4 * half_lane);
         for (int s = 0; s < 2; ++s)
-          tma_gather4(sm + base_off + st * 16384 + s * 8192 + half_lane * 512, mapq, bar_qf + st,
+          tma_gather4(sm + base_off + st * 16384 + s * 8192 + half_lane * 512, mapq,
+                      lane < 16 ? bar_qf + st : bar_df + st,
                       head * D + s * 64, r.x, r.y, r.z, r.w);
       }
     } else if (warp == 0) {
@@ -596,17 +625,32 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         mbar_wait(bar_qe + st, ((i / Ly::kStages) & 1) ^ 1);
         if (((OSP_BWD_EXPERIMENTS ? a.flags : 0) & 64) && i >= 2) {  // experiment 64: no Q/dO reloads (stale tiles, timing only)
           mbar_arrive(bar_qf + st);
+          if (OSP_BWD_SPLITQ) mbar_arrive(bar_df + st);
           continue;
         }
-        mbar_expect_tx(bar_qf + st, 2 * 16384 + 512);
-        for (int s = 0; s < 2; ++s) {
-          tma_load_3d(sm + Ly::kQ + st * 16384 + s * 8192, &tmQ, bar_qf + st, head * D + s * 64,
-                      i * 64, seq);
-          tma_load_3d(sm + Ly::kDO + st * 16384 + s * 8192, &tmDO, bar_qf + st, head * D + s * 64,
-                      i * 64, seq);
+        if (OSP_BWD_SPLITQ) {
+          // Q and its row statistics first (S^T_i needs them), dO after on its own barrier
+          mbar_expect_tx(bar_qf + st, 16384 + 512);
+          for (int s = 0; s < 2; ++s)
+            tma_load_3d(sm + Ly::kQ + st * 16384 + s * 8192, &tmQ, bar_qf + st, head * D + s * 64,
+                        i * 64, seq);
+          bulk_load(sm + Ly::kStat + st * 512, lse2_g + i * 64, 256, bar_qf + st);
+          bulk_load(sm + Ly::kStat + st * 512 + 256, delta_g + i * 64, 256, bar_qf + st);
+          mbar_expect_tx(bar_df + st, 16384);
+          for (int s = 0; s < 2; ++s)
+            tma_load_3d(sm + Ly::kDO + st * 16384 + s * 8192, &tmDO, bar_df + st, head * D + s * 64,
+                        i * 64, seq);
+        } else {
+          mbar_expect_tx(bar_qf + st, 2 * 16384 + 512);
+          for (int s = 0; s < 2; ++s) {
+            tma_load_3d(sm + Ly::kQ + st * 16384 + s * 8192, &tmQ, bar_qf + st, head * D + s * 64,
+                        i * 64, seq);
+            tma_load_3d(sm + Ly::kDO + st * 16384 + s * 8192, &tmDO, bar_qf + st, head * D + s * 64,
+                        i * 64, seq);
+          }
+          bulk_load(sm + Ly::kStat + st * 512, lse2_g + i * 64, 256, bar_qf + st);
+          bulk_load(sm + Ly::kStat + st * 512 + 256, delta_g + i * 64, 256, bar_qf + st);
         }
-        bulk_load(sm + Ly::kStat + st * 512, lse2_g + i * 64, 256, bar_qf + st);
-        bulk_load(sm + Ly::kStat + st * 512 + 256, delta_g + i * 64, 256, bar_qf + st);
       }
       }
       __syncwarp();
@@ -636,6 +680,10 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       };
       auto issue_dp = [&](int i) {
         const uint32_t db = do_base0 + (i % Ly::kStages) * 16384;
+        if (OSP_BWD_SPLITQ) {
+          mbar_wait(bar_df + i % Ly::kStages, (i / Ly::kStages) & 1);
+          tc_fence_after();
+        }
         {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
@@ -657,7 +705,14 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         const uint32_t qb = q_base0 + st * 16384;
         const uint32_t db = do_base0 + st * 16384;
         // dV += P^T dO
+#if OSP_BWD_TIMING
+        long long t0 = clock64();
+#define OSP_BT(k) do { const long long _t = clock64(); atomicAdd(&g_bwd_counters[k], static_cast<unsigned long long>(_t - t0)); t0 = _t; } while (0)
+#else
+#define OSP_BT(k) do { } while (0)
+#endif
         mbar_wait(bar_p, i & 1);
+        OSP_BT(0);
         tc_fence_after();
         {
 #pragma unroll
@@ -667,12 +722,20 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         }
         // S_{i+1} (tS is free once dV_i has been issued: tcgen05 ops execute in order)
         if (i + 1 < n_q) {
+#if OSP_BWD_TIMING
+          t0 = clock64();
+#endif
           mbar_wait(bar_qf + (i + 1) % Ly::kStages, ((i + 1) / Ly::kStages) & 1);
+          OSP_BT(1);
           tc_fence_after();
           issue_s(i + 1);
         }
         // dK += dS^T Q
+#if OSP_BWD_TIMING
+        t0 = clock64();
+#endif
         mbar_wait(bar_ds + b, (i >> 1) & 1);
+        OSP_BT(2);
         tc_fence_after();
         const uint32_t dsb = ds_base + b * 16384;
         {
@@ -685,7 +748,11 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         }
         // dQ^T_i = K^T dS_i^T (single TMEM buffer; the writers drain it right after it lands)
         if (i >= 1) {
+#if OSP_BWD_TIMING
+          t0 = clock64();
+#endif
           mbar_wait(bar_dqf, (i - 1) & 1);
+          OSP_BT(3);
           tc_fence_after();
         }
         {
@@ -697,6 +764,9 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
           tc_commit(bar_dsf + b);
         }
         if (i + 1 < n_q) issue_dp(i + 1);
+#if OSP_BWD_TIMING
+        atomicAdd(&g_bwd_counters[7], 1ull);
+#endif
       }
       tc_commit(bar_fin);
       }
@@ -1158,6 +1228,15 @@ size_t attn_bwd_workspace_bytes(const AttnShape& s) {
   const int64_t a = ((s.n_seq * seq_pad * s.heads * s.head_dim * 4 + 255) / 256) * 256;
   const int64_t b = ((s.n_seq * s.heads * seq_pad * 4 + 255) / 256) * 256;
   return static_cast<size_t>(a + 2 * b);
+}
+
+int debug_counters_bwd(unsigned long long* host, int n, int reset) {
+  if (n > 64) n = 64;
+  int rc = check_cuda(cudaMemcpyFromSymbol(host, g_bwd_counters, n * sizeof(unsigned long long)),
+                      "cudaMemcpyFromSymbol");
+  if (rc != kOk || !reset) return rc;
+  static const unsigned long long zeros[64] = {};
+  return check_cuda(cudaMemcpyToSymbol(g_bwd_counters, zeros, sizeof(zeros)), "cudaMemcpyToSymbol");
 }
 
 int launch_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,
