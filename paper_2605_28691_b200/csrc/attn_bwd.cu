@@ -31,6 +31,11 @@
 
 // Phase timing (-DOSP_BWD_TIMING=1 builds only): clock64 sums of the v2 kernel's MMA issuer waits
 // and of the first compute / writer warp's phases, read back with osp_debug_counters_bwd().
+// dK / dV epilogue through a shared-memory stage with whole-row coalesced stores (1), or one
+// row per thread straight from registers (0, rounds 1-2).
+#ifndef OSP_BWD_STAGED_EPI
+#define OSP_BWD_STAGED_EPI 1
+#endif
 #ifndef OSP_BWD_TIMING
 #define OSP_BWD_TIMING 0
 #endif
@@ -520,6 +525,10 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
     return;
   }
   const int n_q = (len + 63) / 64;
+#if OSP_BWD_TIMING
+  const long long t_entry = clock64();
+  long long t_first = 0, t_fin = 0;
+#endif
 
   if ((smem_u32(sm) & 1023) != 0) __trap();
   if (threadIdx.x == 0) {
@@ -697,6 +706,9 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       mbar_wait(bar_kt, 0);
       mbar_wait(bar_qf + 0, 0);
       tc_fence_after();
+#if OSP_BWD_TIMING
+      t_first = clock64();
+#endif
       issue_s(0);
       issue_dp(0);
       for (int i = 0; i < n_q; ++i) {
@@ -769,6 +781,9 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
 #endif
       }
       tc_commit(bar_fin);
+#if OSP_BWD_TIMING
+      t_fin = clock64();
+#endif
       }
       __syncwarp();
     }
@@ -894,6 +909,43 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         a.row_index ? (kglob < len ? a.row_index[static_cast<int64_t>(seq) * a.seq_len + kglob] : -1)
                     : (kglob < a.seq_len ? static_cast<int64_t>(seq) * a.seq_len + kglob : -1);
     const bool row_ok = out_row >= 0;
+#if OSP_BWD_STAGED_EPI
+    {
+      // Staged through the K (dV) / V (dK) buffers, free once bar_fin has fired: the warp's 32
+      // rows go to its quarter with 16-byte chunks XOR-swizzled by row, then out two whole
+      // 256-byte rows per store instruction instead of 16 bytes of 32 different rows.
+      const int which = half;
+      const uint32_t base = (which == 0 ? tDV : tDK) + la;
+      const float mul = which == 0 ? 1.f : a.scale;
+      uint8_t* stg = sm + (which == 0 ? Ly::kK : Ly::kV) + wq * 8192;
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t o[32];
+        tmem_ld32(base + cc * 32, o);
+        tmem_wait_ld(o);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint4 pk;
+          pk.x = pack_bf16(__uint_as_float(o[8 * i + 0]) * mul, __uint_as_float(o[8 * i + 1]) * mul);
+          pk.y = pack_bf16(__uint_as_float(o[8 * i + 2]) * mul, __uint_as_float(o[8 * i + 3]) * mul);
+          pk.z = pack_bf16(__uint_as_float(o[8 * i + 4]) * mul, __uint_as_float(o[8 * i + 5]) * mul);
+          pk.w = pack_bf16(__uint_as_float(o[8 * i + 6]) * mul, __uint_as_float(o[8 * i + 7]) * mul);
+          *reinterpret_cast<uint4*>(stg + lane * 256 + (((cc * 4 + i) ^ (lane & 15)) * 16)) = pk;
+        }
+      }
+      __syncwarp();
+      __nv_bfloat16* out = (which == 0 ? a.dv : a.dk) + static_cast<int64_t>(head) * D;
+      const int64_t ostride = which == 0 ? a.dv_stride : a.dk_stride;
+      const int ch = lane & 15;
+#pragma unroll 4
+      for (int rr = 0; rr < 16; ++rr) {
+        const int r = 2 * rr + (lane >> 4);
+        const long long dst_row = __shfl_sync(0xFFFFFFFFu, static_cast<long long>(out_row), r);
+        const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 256 + ((ch ^ (r & 15)) * 16));
+        if (dst_row >= 0) *reinterpret_cast<uint4*>(out + dst_row * ostride + ch * 8) = v;
+      }
+    }
+#else
     {
       const int which = half;
       const uint32_t base = (which == 0 ? tDV : tDK) + la;
@@ -917,6 +969,7 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
         }
       }
     }
+#endif
   } else {
     regs_dec<88>();
     // ------------------------------------------------------------------ dQ^T writer warps (thread = d)
@@ -970,6 +1023,16 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
 
   tc_fence_before();
   __syncthreads();
+#if OSP_BWD_TIMING
+  // per CTA, on the MMA issuer's lane: entry -> first S^T issue (prologue), the query-tile loop,
+  // last issue -> every warp done (epilogue: dK/dV drain, the last dQ reductions)
+  if (t_first != 0) {
+    atomicAdd(&g_bwd_counters[8], static_cast<unsigned long long>(t_first - t_entry));
+    atomicAdd(&g_bwd_counters[9], static_cast<unsigned long long>(t_fin - t_first));
+    atomicAdd(&g_bwd_counters[10], static_cast<unsigned long long>(clock64() - t_fin));
+    atomicAdd(&g_bwd_counters[11], 1ull);
+  }
+#endif
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);

@@ -106,6 +106,11 @@ __device__ __forceinline__ bool bit_at(const uint32_t* bits, int words, int i) {
 
 // Phase timing (-DOSP_FWD_TIMING=1 builds only): per-phase clock64 sums of the first softmax
 // warp of each warpgroup and of the MMA issuer, read back with osp_debug_counters().
+// Epilogue through a shared-memory stage with whole-row coalesced stores (1) or one row per
+// thread straight from registers (0, round 1-2).
+#ifndef OSP_FWD_STAGED_EPI
+#define OSP_FWD_STAGED_EPI 1
+#endif
 #ifndef OSP_FWD_TIMING
 #define OSP_FWD_TIMING 0
 #endif
@@ -169,6 +174,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     return;
   }
   const int n_kv = (len + kBN - 1) / kBN;
+#if OSP_FWD_TIMING
+  const long long t_entry = clock64();
+  long long t_first = 0, t_fin = 0;
+#endif
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -333,6 +342,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     mbar_wait(bar_q + 1, 0);
     tc_fence_after();
 #if OSP_FWD_TIMING
+    t_first = clock64();
     unsigned long long mt[4] = {0, 0, 0, 0};
     long long m0 = clock64();
 #define OSP_MT(k) do { const long long _t = clock64(); mt[k] += _t - m0; m0 = _t; } while (0)
@@ -371,6 +381,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #endif
     const int last = n_kv - 1;
     pv(1, last % kFwdVStages, last > 0, last & 1, bar_ve + last % kFwdVStages, bar_o + 0, bar_o + 1);
+#if OSP_FWD_TIMING
+    t_fin = clock64();
+#endif
     }
     __syncwarp();
   }
@@ -595,6 +608,43 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tab ? (row_ok ? __ldg(tab + static_cast<int64_t>(seq) * a.seq_len + q_row) : -1)
             : static_cast<int64_t>(seq) * a.seq_len + q_row;
     const bool write_o = tab ? out_row >= 0 : in_cap;
+#if OSP_FWD_STAGED_EPI
+    // The warp's 32 rows are staged in its quarter of this tile's Q buffer (free: bar_o follows
+    // the last MMA, and tcgen05 ops complete in order), 16-byte chunks XOR-swizzled by row so
+    // both passes are bank-conflict free, then stored two whole 256-byte rows per instruction
+    // instead of one 16-byte piece of 32 different rows.
+    constexpr int kCh = D / 8;               // 16-byte chunks per row
+    constexpr int kRowsPerIns = 32 / kCh;    // rows per coalesced warp store
+    uint8_t* stg = sm + Ly::kQ + t * Ly::kTile + wq * (32 * D * 2);
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld32(tO + cc * 32, o);
+      tmem_wait_ld(o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 pk;
+        pk.x = pack_bf16(__uint_as_float(o[8 * i + 0]) * inv_l, __uint_as_float(o[8 * i + 1]) * inv_l);
+        pk.y = pack_bf16(__uint_as_float(o[8 * i + 2]) * inv_l, __uint_as_float(o[8 * i + 3]) * inv_l);
+        pk.z = pack_bf16(__uint_as_float(o[8 * i + 4]) * inv_l, __uint_as_float(o[8 * i + 5]) * inv_l);
+        pk.w = pack_bf16(__uint_as_float(o[8 * i + 6]) * inv_l, __uint_as_float(o[8 * i + 7]) * inv_l);
+        *reinterpret_cast<uint4*>(stg + lane * (D * 2) + (((cc * 4 + i) ^ (lane & (kCh - 1))) * 16)) = pk;
+      }
+    }
+    __syncwarp();
+    {
+      const int ch = lane % kCh;
+#pragma unroll 4
+      for (int rr = 0; rr < 32 / kRowsPerIns; ++rr) {
+        const int r = kRowsPerIns * rr + lane / kCh;
+        const long long dst_row = __shfl_sync(0xFFFFFFFFu, static_cast<long long>(out_row), r);
+        const bool w = __shfl_sync(0xFFFFFFFFu, write_o ? 1 : 0, r) != 0;
+        const uint4 v = *reinterpret_cast<const uint4*>(stg + r * (D * 2) + ((ch ^ (r & (kCh - 1))) * 16));
+        if (w)
+          *reinterpret_cast<uint4*>(a.o + dst_row * a.o_stride + static_cast<int64_t>(head) * D + ch * 8) = v;
+      }
+    }
+#else
     __nv_bfloat16* orow = a.o + out_row * a.o_stride + static_cast<int64_t>(head) * D;
 #pragma unroll
     for (int cc = 0; cc < D / 32; ++cc) {
@@ -612,6 +662,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int i = 0; i < 4; ++i) dst[i] = pk[i];
       }
     }
+#endif
     if (in_cap) {
       const float ms = (m_used == -INFINITY) ? 0.f : m_used * c;
       a.lse[(static_cast<int64_t>(seq) * a.heads + head) * a.seq_len + q_row] =
@@ -621,6 +672,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+#if OSP_FWD_TIMING
+  // per CTA, on the MMA issuer's lane: entry -> Q landed (prologue), the key loop, last PV issued
+  // -> every warp done (epilogue)
+  if (t_first != 0) {
+    atomicAdd(&g_fwd_counters[24], static_cast<unsigned long long>(t_first - t_entry));
+    atomicAdd(&g_fwd_counters[25], static_cast<unsigned long long>(t_fin - t_first));
+    atomicAdd(&g_fwd_counters[26], static_cast<unsigned long long>(clock64() - t_fin));
+    atomicAdd(&g_fwd_counters[27], 1ull);
+  }
+#endif
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);

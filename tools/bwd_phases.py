@@ -11,7 +11,8 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2605_28691_b200 import _lib, kernels  # noqa: E402
 
-n, L, heads, d = 4, int(sys.argv[1]) if len(sys.argv) > 1 else 20160, 40, 128
+L = int(sys.argv[1]) if len(sys.argv) > 1 else 20160
+n, heads, d = int(sys.argv[2]) if len(sys.argv) > 2 else 4, 40, 128
 C = heads * d
 qkv = torch.randn(n, L, 3 * C, device="cuda").bfloat16()
 do = torch.randn(n, L, C, device="cuda").bfloat16()
@@ -34,3 +35,6 @@ tiles = max(c[7], 1)
 print(f"bwd {e0.elapsed_time(e1):.2f} ms, {tiles} query tiles over all CTAs")
 names = ["wait P", "wait next Q/dO", "wait dS", "wait dQ drained"]
 print("MMA issuer cycles per query tile: " + ", ".join(f"{nm} {c[i] / tiles:.0f}" for i, nm in enumerate(names)))
+ctas = max(c[11], 1)
+print(f"per CTA ({c[11]} CTAs, {tiles / ctas:.1f} query tiles each): prologue {c[8] / ctas:.0f}, "
+      f"loop {c[9] / ctas:.0f}, epilogue {c[10] / ctas:.0f} cycles")

@@ -11,7 +11,8 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2605_28691_b200 import _lib, kernels  # noqa: E402
 
-n, L, heads, d = 4, int(sys.argv[1]) if len(sys.argv) > 1 else 20160, 40, 128
+L = int(sys.argv[1]) if len(sys.argv) > 1 else 20160
+n, heads, d = int(sys.argv[2]) if len(sys.argv) > 2 else 4, 40, 128
 C = heads * d
 qkv = torch.randn(n, L, 3 * C, device="cuda").bfloat16()
 q, k, v = qkv[..., :C], qkv[..., C:2 * C], qkv[..., 2 * C:]
@@ -37,3 +38,6 @@ for t in range(2):
 tiles = max(c[20], 1)
 mn = ["wait K", "wait P1", "wait V", "wait P0"]
 print("MMA issuer: cycles/tile " + ", ".join(f"{nm} {c[16 + i] / tiles:.0f}" for i, nm in enumerate(mn)))
+ctas = max(c[27], 1)
+print(f"per CTA ({c[27]} CTAs, {c[20] / ctas:.1f} key tiles each): prologue {c[24] / ctas:.0f}, "
+      f"loop {c[25] / ctas:.0f}, epilogue {c[26] / ctas:.0f} cycles")

@@ -1,4 +1,5 @@
-// Microbenchmark: MUFU.EX2 vs polynomial exp2 (FMA pipe) throughput per SM.
+// Microbenchmark: MUFU.EX2 vs polynomial exp2 (FMA pipe) throughput per SM, and the packed
+// half-precision forms (ex2.approx.f16x2 / .ftz.bf16x2 lower to two MUFU.EX2.F16 / .BF16 each).
 #include <cstdio>
 #include "../paper_2605_28691_b200/csrc/osp_common.cuh"
 using namespace osp;
@@ -12,6 +13,39 @@ __device__ __forceinline__ float poly1(float x) {
   p = fmaf(p, f, 0.69328293f);
   p = fmaf(p, f, 1.0f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+__device__ __forceinline__ unsigned ex2h2(unsigned h) {
+  unsigned r;
+  asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(h));
+  return r;
+}
+__device__ __forceinline__ unsigned ex2b2(unsigned h) {
+  unsigned r;
+  asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(r) : "r"(h));
+  return r;
+}
+
+// MODE 2: f16x2, MODE 3: bf16x2 -- 16 packed registers = 32 exps per iteration
+template <int MODE>
+__global__ void __launch_bounds__(256) kh(float* out, int iters, long long* cyc) {
+  unsigned v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = 0xBC00BC00u ^ (threadIdx.x + i);
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      unsigned r = MODE == 2 ? ex2h2(v[i]) : ex2b2(v[i]);
+      v[i] = r ^ 0x80008000u;   // keep the arguments negative and dependent
+    }
+  }
+  long long t1 = clock64();
+  unsigned s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += v[i];
+  if (s == 12345u) out[0] = s;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
 }
 
 template <int MODE>
@@ -48,7 +82,20 @@ void run(int threads) {
   printf("%s threads=%d: %.1f exp2/clk/SM\n", MODE == 0 ? "MUFU.EX2" : "poly   ", threads,
          double(threads) * iters * 16 / double(cyc));
 }
+template <int MODE>
+void runh(int threads) {
+  float* o; long long* c;
+  cudaMalloc(&o, 4); cudaMalloc(&c, 8);
+  const int iters = 4000;
+  kh<MODE><<<148, threads>>>(o, 10, c);
+  cudaDeviceSynchronize();
+  kh<MODE><<<148, threads>>>(o, iters, c);
+  cudaDeviceSynchronize();
+  long long cyc; cudaMemcpy(&cyc, c, 8, cudaMemcpyDeviceToHost);
+  printf("%s threads=%d: %.1f exp2/clk/SM\n", MODE == 2 ? "f16x2  " : "bf16x2 ", threads,
+         double(threads) * iters * 32 / double(cyc));
+}
 int main() {
-  for (int t : {128, 256}) { run<0>(t); run<1>(t); }
+  for (int t : {128, 256}) { run<0>(t); run<1>(t); runh<2>(t); runh<3>(t); }
   return 0;
 }
