@@ -33,6 +33,11 @@
 // and of the first compute / writer warp's phases, read back with osp_debug_counters_bwd().
 // dK / dV epilogue through a shared-memory stage with whole-row coalesced stores (1), or one
 // row per thread straight from registers (0, rounds 1-2).
+// K into TMEM copied from the TMA-landed K tile by both compute warpgroups, with the K / V TMA
+// issued at barrier init (1); or K rows read from global by warpgroup 0 after setup (0, rounds 1-2).
+#ifndef OSP_BWD_EARLY_K
+#define OSP_BWD_EARLY_K 1
+#endif
 #ifndef OSP_BWD_STAGED_EPI
 #define OSP_BWD_STAGED_EPI 1
 #endif
@@ -550,6 +555,15 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
     mbar_init(bar_fin, 1);
     mbar_init(bar_kt, 256);
     fence_barrier_init();
+#if OSP_BWD_EARLY_K
+    if (!a.row_index) {  // K / V tiles in flight before the TMEM allocation and the block barrier
+      mbar_expect_tx(bar_kv, 65536);
+      for (int s2 = 0; s2 < 2; ++s2) {
+        tma_load_3d(sm + Ly::kK + s2 * 16384, &tmK, bar_kv, head * D + s2 * 64, kv0, seq);
+        tma_load_3d(sm + Ly::kV + s2 * 16384, &tmV, bar_kv, head * D + s2 * 64, kv0, seq);
+      }
+    }
+#endif
   }
   if (warp == 2) {
     tmem_alloc(tmem_slot, 512);
@@ -622,10 +636,12 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
       tma_prefetch(&tmDO);
-      mbar_expect_tx(bar_kv, 65536);
-      for (int s = 0; s < 2; ++s) {
-        tma_load_3d(sm + Ly::kK + s * 16384, &tmK, bar_kv, head * D + s * 64, kv0, seq);
-        tma_load_3d(sm + Ly::kV + s * 16384, &tmV, bar_kv, head * D + s * 64, kv0, seq);
+      if (!OSP_BWD_EARLY_K) {
+        mbar_expect_tx(bar_kv, 65536);
+        for (int s = 0; s < 2; ++s) {
+          tma_load_3d(sm + Ly::kK + s * 16384, &tmK, bar_kv, head * D + s * 64, kv0, seq);
+          tma_load_3d(sm + Ly::kV + s * 16384, &tmV, bar_kv, head * D + s * 64, kv0, seq);
+        }
       }
       const float* lse2_g = a.lse2 + sh * a.seq_pad;
       const float* delta_g = a.delta + sh * a.seq_pad;
@@ -801,12 +817,31 @@ __global__ void __launch_bounds__(kBwdV2Threads, 1)
       const uint32_t* vb = a.valid_bits + static_cast<int64_t>(seq) * a.words_per_seq;
       kvalid = (__ldg(vb + (kglob >> 5)) >> (kglob & 31)) & 1u;
     }
+#if OSP_BWD_EARLY_K
+    {
+      // K into TMEM from the TMA-landed K tile (128B-swizzled: 16-byte chunk c of row r at
+      // c ^ (r & 7)); warpgroup h copies columns [64h, 64h + 64) of its key row
+      mbar_wait(bar_kv, 0);
+      const uint8_t* src = sm + Ly::kK + half * 16384 + krow * 128;
+      uint32_t r[32];
+#pragma unroll
+      for (int c2 = 0; c2 < 8; ++c2) {
+        const uint4 v = *reinterpret_cast<const uint4*>(src + ((c2 ^ (krow & 7)) * 16));
+        r[4 * c2 + 0] = v.x;
+        r[4 * c2 + 1] = v.y;
+        r[4 * c2 + 2] = v.z;
+        r[4 * c2 + 3] = v.w;
+      }
+      tmem_st32(tK + la + half * 32, r);
+    }
+#else
     if (half == 0)
       row_to_tmem(tK + la,
                   a.k_rows + (a.row_index ? (kglob < len ? static_cast<int64_t>(a.row_index[static_cast<int64_t>(seq) * a.seq_len + kglob]) : 0)
                                           : static_cast<int64_t>(seq) * a.seq_len + kglob) * a.k_row_stride +
                       static_cast<int64_t>(head) * D,
                   kglob < len);
+#endif
     tmem_wait_st();
     tc_fence_before();
     mbar_arrive(bar_kt);

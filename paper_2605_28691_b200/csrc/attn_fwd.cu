@@ -108,6 +108,11 @@ __device__ __forceinline__ bool bit_at(const uint32_t* bits, int words, int i) {
 // warp of each warpgroup and of the MMA issuer, read back with osp_debug_counters().
 // Epilogue through a shared-memory stage with whole-row coalesced stores (1) or one row per
 // thread straight from registers (0, round 1-2).
+// Q tiles requested by thread 0 right after the barrier init (1), or by the producer after the
+// block barrier (0, rounds 1-2).
+#ifndef OSP_FWD_EARLY_Q
+#define OSP_FWD_EARLY_Q 1
+#endif
 #ifndef OSP_FWD_STAGED_EPI
 #define OSP_FWD_STAGED_EPI 1
 #endif
@@ -195,6 +200,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(bar_ve + i, 1);
     }
     fence_barrier_init();
+#if OSP_FWD_EARLY_Q
+    if (!a.row_index) {  // the Q tiles in flight before the TMEM allocation and the block barrier
+      for (int t = 0; t < 2; ++t) {
+        mbar_expect_tx(bar_q + t, Ly::kTile);
+#pragma unroll
+        for (int s = 0; s < Ly::kSub; ++s)
+          tma_load_3d(sm + Ly::kQ + t * Ly::kTile + s * 16384, &tmQ, bar_q + t, head * D + s * 64,
+                      q_row0 + t * kBM, seq);
+      }
+    }
+#endif
   }
   if (warp == 2) {
     tmem_alloc(tmem_slot, 512);
@@ -248,7 +264,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tma_prefetch(&tmQ);
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
-      for (int t = 0; t < 2; ++t) {
+      for (int t = 0; t < 2 && !OSP_FWD_EARLY_Q; ++t) {
         mbar_expect_tx(bar_q + t, Ly::kTile);
 #pragma unroll
         for (int s = 0; s < Ly::kSub; ++s)
