@@ -17,7 +17,12 @@ want = [r"^Kernel Name$", r"^gpu__time_duration.sum$", r"^dram__bytes_(read|writ
         r"^lts__throughput.avg.pct_of_peak_sustained_elapsed$",
         r"^dram__throughput.avg.pct_of_peak_sustained_elapsed$",
         r"^launch__(registers_per_thread|grid_size|block_size)$",
-        r"^sm__cycles_elapsed.avg.per_second$"]
+        r"^sm__cycles_elapsed.avg.per_second$",
+        r"^l1tex__throughput.avg.pct_of_peak_sustained_active$",
+        r"^l1tex__data_pipe_(tc|lsu)_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed$",
+        r"^l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum$",
+        r"^l1tex__m_l1tex2xbar_write_bytes_mem_global_op_tma_red.sum$",
+        r"^l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum$"]
 for r in rows[2:]:
     print("----")
     for i, h in enumerate(hdr):
