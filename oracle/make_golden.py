@@ -3,7 +3,7 @@
 TEST INFRASTRUCTURE ONLY.  Run in the build container, where the reference is
 mounted read-only:
 
-    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden.py
+    PYTHONDONTWRITEBYTECODE=1 python oracle/make_golden.py [report]
 
 It imports /root/reference/pkg/src/osp (never copied into this repo), calls
 its public functions on small seeded inputs and stores inputs + outputs as
@@ -233,8 +233,20 @@ def hif8_golden():
     np.savez_compressed(OUT / "hif8.npz", **arrays)
 
 
+def report_golden():
+    """The reference's `report-all` document for seed 0 (cli.py:279-325), which
+    paper_2605_28691_b200.report reproduces section by section on the device."""
+    from osp.cli import build_full_report
+    text = json.dumps(build_full_report(0), indent=2, sort_keys=True) + "\n"
+    (OUT / "report_all_seed0.json").write_text(text)
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
+    if sys.argv[1:] == ["report"]:      # only the report-all document
+        report_golden()
+        return
+    report_golden()
     formats_golden()
     hif8_golden()
     a_maps, m_maps = maps_golden()
