@@ -36,11 +36,19 @@ namespace {
 constexpr int kPBM = 128, kPBN = 256, kPBK = 64, kPStages = 4;
 constexpr int kPThreads = 256;
 
+// Epilogue rows staged in shared memory and stored as whole coalesced rows (1), or one row per
+// thread straight from registers (0, rounds 1-2).
+#ifndef OSP_PROJ_STAGED_EPI
+#define OSP_PROJ_STAGED_EPI 1
+#endif
+constexpr int kPStage = OSP_PROJ_STAGED_EPI ? 4 * 32 * 256 : 0;  // 4 epilogue warps x 32 rows x 256 B
+
 struct ProjLayout {
   static constexpr int kA = 0;                                   // stages x 16 KB
   static constexpr int kB = kPStages * kPBM * kPBK * 2;          // stages x 32 KB
   static constexpr int kBar = kB + kPStages * kPBN * kPBK * 2;
-  static constexpr int kSmem = kBar + 256;
+  static constexpr int kStg = kBar + 1024;
+  static constexpr int kSmem = kStg + kPStage;
 };
 
 // CTA-pair variant: per stage each CTA holds its 128 x rows and its 128-row half of the W slice
@@ -49,8 +57,10 @@ struct Proj2Layout {
   static constexpr int kA = 0;                                   // stages x 16 KB
   static constexpr int kB = kP2Stages * kPBM * kPBK * 2;         // stages x 16 KB (W half)
   static constexpr int kBar = kB + kP2Stages * (kPBN / 2) * kPBK * 2;
-  static constexpr int kSmem = kBar + 256;
+  static constexpr int kStg = kBar + 1024;
+  static constexpr int kSmem = kStg + kPStage;
 };
+static_assert(Proj2Layout::kSmem <= 232448 && ProjLayout::kSmem <= 232448, "K6 shared memory");
 
 struct ProjArgs {
   __nv_bfloat16* out;
@@ -316,6 +326,30 @@ __global__ void __launch_bounds__(kPThreads, 1)
                           a.rope != nullptr);
           }
         }
+#if OSP_PROJ_STAGED_EPI
+        {
+          // the warp's 32 rows x 128 columns go through its 8 KB stage (16-byte chunks
+          // XOR-swizzled by row: both passes bank-conflict free), then out two whole 256-byte
+          // rows per store instruction
+          uint8_t* stg = sm + Ly::kStg + wq * 8192;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            *reinterpret_cast<uint4*>(stg + lane * 256 + ((j ^ (lane & 15)) * 16)) =
+                make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                           pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+          __syncwarp();
+          const int ch = lane & 15;
+          const int row0 = tm * kPBM + wq * 32;
+#pragma unroll 4
+          for (int rr = 0; rr < 16; ++rr) {
+            const int r = 2 * rr + (lane >> 4);
+            if (row0 + r < a.rows)
+              *reinterpret_cast<uint4*>(a.out + static_cast<int64_t>(row0 + r) * a.out_stride + c0 + ch * 8) =
+                  *reinterpret_cast<const uint4*>(stg + r * 256 + ((ch ^ (r & 15)) * 16));
+          }
+          __syncwarp();
+        }
+#else
         if (row_ok) {
           uint4* dst = reinterpret_cast<uint4*>(a.out + static_cast<int64_t>(row) * a.out_stride + c0);
 #pragma unroll
@@ -323,6 +357,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             dst[j] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
                                 pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
         }
+#endif
       }
     }
   }
