@@ -38,6 +38,10 @@ constexpr int kPThreads = 256;
 
 // Epilogue rows staged in shared memory and stored as whole coalesced rows (1), or one row per
 // thread straight from registers (0, rounds 1-2).
+// L2 policy: the W band's TMA loads evict-last, output stores streaming (1), or default (0).
+#ifndef OSP_PROJ_L2HINT
+#define OSP_PROJ_L2HINT 1
+#endif
 #ifndef OSP_PROJ_STAGED_EPI
 #define OSP_PROJ_STAGED_EPI 1
 #endif
@@ -215,6 +219,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     if (elect_one()) {
       tma_prefetch(&tmA);
       tma_prefetch(&tmB);
+      const uint64_t pol_w = l2_policy_evict_last();
+      (void)pol_w;
       int it = 0;
       for (int id = cluster; id < n_units; id += n_clusters) {
         int tm, tn;
@@ -226,9 +232,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
             // both CTAs' A and W halves complete on the leader's full barrier
             const uint32_t leader_full = mapa_u32(smem_u32(bar_full + st), 0);
             if (crank == 0) mbar_expect_tx(bar_full + st, 2 * (kPBM + kBRows) * kPBK * 2);
-            tma_load_3d_pair(sm + Ly::kA + st * kPBM * kPBK * 2, &tmA, leader_full, ks * kPBK, tm * kPBM, 0);
-            tma_load_3d_pair(sm + Ly::kB + st * kBRows * kPBK * 2, &tmB, leader_full, ks * kPBK,
-                             tn * kPBN + static_cast<int>(crank) * kBRows, 0);
+            if (OSP_PROJ_L2HINT) {
+              // the band's W slice is reused by every row pair of the band: keep it in L2
+              tma_load_3d_pair(sm + Ly::kA + st * kPBM * kPBK * 2, &tmA, leader_full, ks * kPBK, tm * kPBM, 0);
+              tma_load_3d_pair_hint(sm + Ly::kB + st * kBRows * kPBK * 2, &tmB, leader_full, ks * kPBK,
+                                    tn * kPBN + static_cast<int>(crank) * kBRows, 0, pol_w);
+            } else {
+              tma_load_3d_pair(sm + Ly::kA + st * kPBM * kPBK * 2, &tmA, leader_full, ks * kPBK, tm * kPBM, 0);
+              tma_load_3d_pair(sm + Ly::kB + st * kBRows * kPBK * 2, &tmB, leader_full, ks * kPBK,
+                               tn * kPBN + static_cast<int>(crank) * kBRows, 0);
+            }
           } else {
             mbar_expect_tx(bar_full + st, (kPBM + kPBN) * kPBK * 2);
             tma_load_3d(sm + Ly::kA + st * kPBM * kPBK * 2, &tmA, bar_full + st, ks * kPBK, tm * kPBM, 0);
@@ -343,9 +356,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll 4
           for (int rr = 0; rr < 16; ++rr) {
             const int r = 2 * rr + (lane >> 4);
-            if (row0 + r < a.rows)
-              *reinterpret_cast<uint4*>(a.out + static_cast<int64_t>(row0 + r) * a.out_stride + c0 + ch * 8) =
-                  *reinterpret_cast<const uint4*>(stg + r * 256 + ((ch ^ (r & 15)) * 16));
+            if (row0 + r < a.rows) {
+              uint4* dst = reinterpret_cast<uint4*>(a.out + static_cast<int64_t>(row0 + r) * a.out_stride + c0 + ch * 8);
+              const uint4 v4 = *reinterpret_cast<const uint4*>(stg + r * 256 + ((ch ^ (r & 15)) * 16));
+              if (OSP_PROJ_L2HINT) __stcs(dst, v4);   // streamed out: do not displace the W band
+              else *dst = v4;
+            }
           }
           __syncwarp();
         }
