@@ -128,6 +128,9 @@ EXTRA = {
     "k4_pad": (3, 30, 20, 4, 2, 128),    # H, W -> 32, 32
     "k2_odd": (1, 13, 17, 2, 1, 64),     # H, W -> 16, 20
     "k2_T5": (5, 8, 12, 2, 4, 64),       # no padding, T > 1
+    "cfg3k4": (21, 45, 80, 4, 40, 128),  # the cfg3 shape at k = 4 (bench --config cfg3k4)
+    "cfg5k2": (33, 45, 80, 2, 40, 128),  # BASELINE config 5, 129 frames (bench --config cfg5k2)
+    "cfg5k4": (33, 45, 80, 4, 40, 128),  # BASELINE config 5 at k = 4
 }
 
 
