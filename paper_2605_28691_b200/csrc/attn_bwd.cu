@@ -29,18 +29,18 @@
 #define OSP_BWD_EXPERIMENTS 0
 #endif
 
-// Phase timing (-DOSP_BWD_TIMING=1 builds only): clock64 sums of the v2 kernel's MMA issuer waits
-// and of the first compute / writer warp's phases, read back with osp_debug_counters_bwd().
-// dK / dV epilogue through a shared-memory stage with whole-row coalesced stores (1), or one
-// row per thread straight from registers (0, rounds 1-2).
 // K into TMEM copied from the TMA-landed K tile by both compute warpgroups, with the K / V TMA
 // issued at barrier init (1); or K rows read from global by warpgroup 0 after setup (0, rounds 1-2).
 #ifndef OSP_BWD_EARLY_K
 #define OSP_BWD_EARLY_K 1
 #endif
+// dK / dV epilogue through a shared-memory stage with whole-row coalesced stores (1), or one
+// row per thread straight from registers (0, rounds 1-2).
 #ifndef OSP_BWD_STAGED_EPI
 #define OSP_BWD_STAGED_EPI 1
 #endif
+// Phase timing (-DOSP_BWD_TIMING=1 builds only): clock64 sums of the v2 kernel's MMA issuer waits
+// and per-CTA prologue / loop / epilogue cycles, read back with osp_debug_counters_bwd().
 #ifndef OSP_BWD_TIMING
 #define OSP_BWD_TIMING 0
 #endif

@@ -104,18 +104,19 @@ __device__ __forceinline__ bool bit_at(const uint32_t* bits, int words, int i) {
   return w < words && ((__ldg(bits + w) >> (i & 31)) & 1u);
 }
 
-// Phase timing (-DOSP_FWD_TIMING=1 builds only): per-phase clock64 sums of the first softmax
-// warp of each warpgroup and of the MMA issuer, read back with osp_debug_counters().
-// Epilogue through a shared-memory stage with whole-row coalesced stores (1) or one row per
-// thread straight from registers (0, round 1-2).
 // Q tiles requested by thread 0 right after the barrier init (1), or by the producer after the
 // block barrier (0, rounds 1-2).
 #ifndef OSP_FWD_EARLY_Q
 #define OSP_FWD_EARLY_Q 1
 #endif
+// Epilogue through a shared-memory stage with whole-row coalesced stores (1) or one row per
+// thread straight from registers (0, rounds 1-2).
 #ifndef OSP_FWD_STAGED_EPI
 #define OSP_FWD_STAGED_EPI 1
 #endif
+// Phase timing (-DOSP_FWD_TIMING=1 builds only): per-phase clock64 sums of the first softmax
+// warp of each warpgroup and of the MMA issuer, and per-CTA prologue / loop / epilogue cycles,
+// read back with osp_debug_counters().
 #ifndef OSP_FWD_TIMING
 #define OSP_FWD_TIMING 0
 #endif
