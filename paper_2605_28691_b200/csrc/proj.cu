@@ -27,7 +27,9 @@
 #include "osp_common.cuh"
 #include "osp_internal.h"
 
+#include <atomic>
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
 
 namespace osp {
@@ -71,6 +73,8 @@ struct ProjArgs {
   int64_t out_stride;
   int rows, chan, n_cols, n_pairs_m, n_tiles_n, k_steps;
   int band;                 // rasterisation: tile pairs per band (all column tiles per band)
+  int* work_counter;        // pair kernel: units handed out in global order by an atomic counter
+                            // (null: each cluster takes units cluster + k * n_clusters)
   int col_bands;            // 1: bands of `band` column tiles over all row pairs instead
   int norm;                 // 0 none, 1 per head, 2 per token (two-phase)
   const float* gamma_q;     // (C) or null
@@ -167,6 +171,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint64_t* bar_acc = bars + 2 * kStages;     // [2] MMA -> epilogue
   uint64_t* bar_accf = bars + 2 * kStages + 2;  // [2] epilogue -> MMA (128, pair: 256 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  // dynamic schedule (pair kernel): a 4-slot ring of unit ids per CTA, filled by the leader's
+  // producer (atomic counter) for both CTAs; bar_uf: id written (1 arrival), bar_ue (leader only):
+  // slot consumed by the leader's MMA issuer and 4 epilogue warps and the peer's producer and 4
+  // epilogue warps (10 arrivals)
+  uint64_t* bar_uf = bars + 2 * kStages + 5;
+  uint64_t* bar_ue = bars + 2 * kStages + 9;
+  int* unit_ring = reinterpret_cast<int*>(bars + 2 * kStages + 13);
+  const bool dyn = kPair && a.work_counter != nullptr;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
@@ -190,6 +202,44 @@ __global__ void __launch_bounds__(kPThreads, 1)
     tn = rem / pairs_in_band;
   };
 
+  // Unit enumeration shared by the three roles.  Static: id = cluster + k * n_clusters.  Dynamic
+  // (pair): units in global order from an atomic counter, so the clusters work on neighbouring
+  // units at any moment however their speeds drift (the W band and the x rows in flight stay
+  // L2-resident, as with a non-persistent launch).  role 0: the leader's producer (draws the id
+  // and publishes it to both CTAs), 1: the leader's MMA issuer, 2: an epilogue warp (whole warp),
+  // 3: the peer's producer.  f(id) is called per unit; returns when the units are exhausted.
+  auto for_each_unit = [&](int role, auto&& f) {
+    if (!dyn) {
+      for (int id = cluster; id < n_units; id += n_clusters) f(id);
+      return;
+    }
+    for (int q = 0;; ++q) {
+      const int slot = q & 3;
+      const uint32_t ph = (q >> 2) & 1;
+      int id;
+      if (role == 0) {
+        mbar_wait(bar_ue + slot, ph ^ 1);
+        id = atomicAdd(a.work_counter, 1);
+        if (id >= n_units) id = -1;
+        unit_ring[slot] = id;
+        st_cluster_u32(mapa_u32(smem_u32(unit_ring + slot), 1), static_cast<uint32_t>(id));
+        mbar_arrive(bar_uf + slot);
+        mbar_arrive_cluster(mapa_u32(smem_u32(bar_uf + slot), 1));
+      } else {
+        mbar_wait(bar_uf + slot, ph);
+        fence_acq_rel_cluster();
+        id = *reinterpret_cast<volatile int*>(unit_ring + slot);
+        if (role == 2) __syncwarp();
+        if (role != 2 || lane == 0) {
+          if (crank == 0) mbar_arrive(bar_ue + slot);
+          else mbar_arrive_cluster(mapa_u32(smem_u32(bar_ue + slot), 0));
+        }
+      }
+      if (id < 0) return;
+      f(id);
+    }
+  };
+
   if ((smem_u32(sm) & 1023) != 0) __trap();
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -199,6 +249,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_acc + i, 1);
       mbar_init(bar_accf + i, kPair ? 256 : 128);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(bar_uf + i, 1);
+      mbar_init(bar_ue + i, 10);
     }
     fence_barrier_init();
   }
@@ -222,7 +276,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const uint64_t pol_w = l2_policy_evict_last();
       (void)pol_w;
       int it = 0;
-      for (int id = cluster; id < n_units; id += n_clusters) {
+      for_each_unit(crank == 0 ? 0 : 3, [&](int id) {
         int tm, tn;
         tile_mn(id, tm, tn);
         for (int ks = 0; ks < a.k_steps; ++ks, ++it) {
@@ -251,14 +305,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                   0x3);
           }
         }
-      }
+      });
     }
     __syncwarp();
   } else if (warp == 1 && (!kPair || crank == 0)) {
     constexpr uint32_t kId = idesc_bf16(kPair ? 2 * kPBM : kPBM, kPBN, 0, 0);
     if (elect_one()) {
       int it = 0, lt = 0;
-      for (int id = cluster; id < n_units; id += n_clusters, ++lt) {
+      for_each_unit(1, [&](int) {
         const int buf = lt & 1;
         if (lt >= 2) mbar_wait(bar_accf + buf, ((lt >> 1) - 1) & 1);
         tc_fence_after();
@@ -287,7 +341,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
           tc_commit_pair(bar_acc + buf, 0x3);
         else
           tc_commit(bar_acc + buf);
-      }
+        ++lt;
+      });
     }
     __syncwarp();
   } else if (warp >= 4) {
@@ -295,7 +350,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const int wq = warp & 3;
     const uint32_t la = static_cast<uint32_t>(wq * 32) << 16;
     int lt = 0;
-    for (int id = cluster; id < n_units; id += n_clusters, ++lt) {
+    for_each_unit(2, [&](int id) {
       int tm, tn;
       tile_mn(id, tm, tn);
       const int buf = lt & 1;
@@ -375,7 +430,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
 #endif
       }
-    }
+      ++lt;
+    });
   }
   tc_fence_before();
   cluster_sync();  // the peer may still multicast into / arrive on this CTA until it is done
@@ -580,6 +636,31 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int n_units = a.n_pairs_m * a.n_tiles_n;
+  // dynamic unit schedule (pair kernel): a work counter zeroed on the stream before the launch;
+  // launches rotate through 64 counters per device, so concurrent launches on other streams do
+  // not share one
+  static const bool dynamic = env_int("OSP_PROJ_DYN", 1) != 0;
+  a.work_counter = nullptr;
+  if (pair && dynamic) {
+    static std::mutex mu;
+    static int* counters[64] = {};
+    static std::atomic<unsigned> seq{0};
+    if (dev < 0 || dev >= 64) {
+      set_error("qkv projection: device index out of range");
+      return kValue;
+    }
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (!counters[dev]) {
+        void* p = nullptr;
+        if ((rc = check_cuda(cudaMalloc(&p, 64 * sizeof(int)), "cudaMalloc(work counters)")) != kOk) return rc;
+        counters[dev] = static_cast<int*>(p);
+      }
+    }
+    a.work_counter = counters[dev] + (seq.fetch_add(1) % 64);
+    if ((rc = check_cuda(cudaMemsetAsync(a.work_counter, 0, sizeof(int), stream), "memset work counter")) != kOk)
+      return rc;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * min(n_units, sms / 2));
   cfg.blockDim = dim3(kPThreads);
