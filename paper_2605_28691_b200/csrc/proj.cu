@@ -44,6 +44,10 @@ constexpr int kPThreads = 256;
 #ifndef OSP_PROJ_L2HINT
 #define OSP_PROJ_L2HINT 1
 #endif
+// Staged epilogue rows leave through TMA stores (1) or coalesced st.global (0).
+#ifndef OSP_PROJ_TMA_STORE
+#define OSP_PROJ_TMA_STORE 1
+#endif
 #ifndef OSP_PROJ_STAGED_EPI
 #define OSP_PROJ_STAGED_EPI 1
 #endif
@@ -159,7 +163,7 @@ __device__ __forceinline__ void head_epilogue(float (&v)[128], const ProjArgs& a
 template <bool kPair>
 __global__ void __launch_bounds__(kPThreads, 1)
     qkv_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const ProjArgs a) {
+                    const __grid_constant__ CUtensorMap tmO, const ProjArgs a) {
   using Ly = std::conditional_t<kPair, Proj2Layout, ProjLayout>;
   constexpr int kStages = kPair ? kP2Stages : kPStages;
   constexpr int kBRows = kPair ? kPBN / 2 : kPBN;   // W rows per CTA per stage
@@ -394,7 +398,30 @@ __global__ void __launch_bounds__(kPThreads, 1)
                           a.rope != nullptr);
           }
         }
-#if OSP_PROJ_STAGED_EPI
+#if OSP_PROJ_STAGED_EPI && OSP_PROJ_TMA_STORE
+        {
+          // the warp's 32 rows x 128 columns go to its 8 KB stage as two 128B-swizzled boxes of
+          // 32 rows x 64 columns, which one lane then hands to two TMA stores (rows past the
+          // matrix are clipped by the tensor map); the stage is rewritten only after the
+          // previous stores have read it
+          uint8_t* stg = sm + Ly::kStg + wq * 8192;
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            *reinterpret_cast<uint4*>(stg + (j >> 3) * 4096 + lane * 128 + (((j & 7) ^ (lane & 7)) * 16)) =
+                make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                           pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int row0 = tm * kPBM + wq * 32;
+            tma_store_3d(&tmO, stg, c0, row0, 0);
+            tma_store_3d(&tmO, stg + 4096, c0 + 64, row0, 0);
+            tma_store_commit();
+          }
+        }
+#elif OSP_PROJ_STAGED_EPI
         {
           // the warp's 32 rows x 128 columns go through its 8 KB stage (16-byte chunks
           // XOR-swizzled by row: both passes bank-conflict free), then out two whole 256-byte
@@ -432,6 +459,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
       ++lt;
     });
+    if (OSP_PROJ_STAGED_EPI && OSP_PROJ_TMA_STORE && lane == 0) tma_store_wait_all();
   }
   tc_fence_before();
   cluster_sync();  // the peer may still multicast into / arrive on this CTA until it is done
@@ -613,6 +641,8 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   CUtensorMap ma, mb;
   if ((rc = make_tmap_bf16_3d(&ma, x, chan, rows, 1, chan, kPBM)) != kOk) return rc;
   if ((rc = make_tmap_bf16_3d(&mb, w_t, chan, n, 1, chan, kPBN / 2)) != kOk) return rc;  // W half
+  CUtensorMap mo;
+  if ((rc = make_tmap_bf16_3d(&mo, out, n, rows, 1, out_stride, 32)) != kOk) return rc;  // epilogue boxes
   static std::atomic<uint64_t> attr_done_1{0}, attr_done_2{0};
   rc = set_smem_attr(reinterpret_cast<const void*>(qkv_gemm_kernel<false>), ProjLayout::kSmem, attr_done_1,
                      "cudaFuncSetAttribute(qkv_gemm)");
@@ -673,8 +703,8 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  rc = check_cuda(pair ? cudaLaunchKernelEx(&cfg, qkv_gemm_kernel<true>, ma, mb, a)
-                       : cudaLaunchKernelEx(&cfg, qkv_gemm_kernel<false>, ma, mb, a),
+  rc = check_cuda(pair ? cudaLaunchKernelEx(&cfg, qkv_gemm_kernel<true>, ma, mb, mo, a)
+                       : cudaLaunchKernelEx(&cfg, qkv_gemm_kernel<false>, ma, mb, mo, a),
                   "qkv_gemm launch");
   if (rc != kOk || norm != 2) return rc;
   const int64_t warps = rows * 2;
