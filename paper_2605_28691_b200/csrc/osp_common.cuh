@@ -235,6 +235,18 @@ __device__ __forceinline__ void tma_load_3d_pair_hint(void* dst, const CUtensorM
       "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
 }
+// cta_group::2 load multicast to the CTAs in cta_mask; each destination pair's leader barrier (at
+// the CTA-relative offset of leader_bar) receives the transaction bytes.
+__device__ __forceinline__ void tma_load_3d_pair_multicast(void* dst, const CUtensorMap* m, uint32_t leader_bar,
+                                                           int c0, int c1, int c2, uint16_t cta_mask,
+                                                           uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6, %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "h"(cta_mask),
+      "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));

@@ -160,7 +160,10 @@ __device__ __forceinline__ void head_epilogue(float (&v)[128], const ProjArgs& a
 // TMA-multicast into both.  kPair = true: the cluster is a CTA pair running cta_group::2 MMAs
 // (M=256 over both CTAs' TMEM, N=256 with each CTA holding a 128-row half of the W slice), issued
 // by the leader CTA; each CTA's TMA lands its operands in its own smem and signals the leader.
-template <bool kPair>
+// kQuad (with kPair): clusters of two such pairs on vertically adjacent row pairs and the same
+// column tile; each CTA loads a quarter of the W slice and multicasts it to its counterpart in the
+// other pair, so the W slice crosses L2 -> SM once per 512 rows (as cuBLAS's 2x1 clusters do).
+template <bool kPair, bool kQuad = false>
 __global__ void __launch_bounds__(kPThreads, 1)
     qkv_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const ProjArgs a) {
@@ -186,23 +189,27 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t crank = cluster_ctarank();
-  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
-  const int n_units = a.n_pairs_m * a.n_tiles_n;  // a unit = two vertically adjacent tiles
+  constexpr int kCtas = kQuad ? 4 : 2;             // CTAs per cluster
+  const uint32_t lead = crank & ~1u;               // this CTA's pair leader (MMA issuer)
+  const int cluster = blockIdx.x / kCtas, n_clusters = gridDim.x / kCtas;
+  // a unit = kCtas vertically adjacent 128-row tiles x one 256-column tile
+  const int n_row_units = kQuad ? (a.n_pairs_m + 1) / 2 : a.n_pairs_m;
+  const int n_units = n_row_units * a.n_tiles_n;
   auto tile_mn = [&](int id, int& tm, int& tn) {
     if (a.col_bands) {  // bands of a.band column tiles swept over all row pairs (W band L2-resident)
-      const int band_units = a.band * a.n_pairs_m;
+      const int band_units = a.band * n_row_units;
       const int band = id / band_units;
       const int rem = id % band_units;
       const int cols_in_band = min(a.band, a.n_tiles_n - band * a.band);
       tn = band * a.band + rem % cols_in_band;
-      tm = 2 * (rem / cols_in_band) + static_cast<int>(crank);
+      tm = kCtas * (rem / cols_in_band) + static_cast<int>(crank);
       return;
     }
     const int band_units = a.band * a.n_tiles_n;
     const int band = id / band_units;
     const int rem = id % band_units;
-    const int pairs_in_band = min(a.band, a.n_pairs_m - band * a.band);
-    tm = 2 * (band * a.band + rem % pairs_in_band) + static_cast<int>(crank);
+    const int pairs_in_band = min(a.band, n_row_units - band * a.band);
+    tm = kCtas * (band * a.band + rem % pairs_in_band) + static_cast<int>(crank);
     tn = rem / pairs_in_band;
   };
 
@@ -226,9 +233,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         id = atomicAdd(a.work_counter, 1);
         if (id >= n_units) id = -1;
         unit_ring[slot] = id;
-        st_cluster_u32(mapa_u32(smem_u32(unit_ring + slot), 1), static_cast<uint32_t>(id));
+        for (uint32_t r = 1; r < kCtas; ++r)
+          st_cluster_u32(mapa_u32(smem_u32(unit_ring + slot), r), static_cast<uint32_t>(id));
         mbar_arrive(bar_uf + slot);
-        mbar_arrive_cluster(mapa_u32(smem_u32(bar_uf + slot), 1));
+        for (uint32_t r = 1; r < kCtas; ++r) mbar_arrive_cluster(mapa_u32(smem_u32(bar_uf + slot), r));
       } else {
         mbar_wait(bar_uf + slot, ph);
         fence_acq_rel_cluster();
@@ -248,7 +256,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(bar_full + i, 1);
-      mbar_init(bar_empty + i, kPair ? 1 : 2);  // multicast: both CTAs' MMAs read the W half
+      // multicast: both CTAs' MMAs read the W half; quad: both pairs' MMAs read my W quarter
+      mbar_init(bar_empty + i, kPair ? (kQuad ? 2 : 1) : 2);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_acc + i, 1);
@@ -256,7 +265,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(bar_uf + i, 1);
-      mbar_init(bar_ue + i, 10);
+      // consumers: the pair leaders' MMA issuers, 4 epilogue warps per CTA, the other producers
+      mbar_init(bar_ue + i, kCtas / 2 + 4 * kCtas + (kCtas - 1));
     }
     fence_barrier_init();
   }
@@ -286,7 +296,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int ks = 0; ks < a.k_steps; ++ks, ++it) {
           const int st = it % kStages;
           mbar_wait(bar_empty + st, ((it / kStages) & 1) ^ 1);
-          if constexpr (kPair) {
+          if constexpr (kQuad) {
+            // my pair leader counts both CTAs' A tiles and W halves; my W half arrives as two
+            // quarters, mine and the one my counterpart in the other pair multicasts
+            const uint32_t leader_full = mapa_u32(smem_u32(bar_full + st), lead);
+            if ((crank & 1) == 0) mbar_expect_tx(bar_full + st, 2 * (kPBM + kBRows) * kPBK * 2);
+            tma_load_3d_pair(sm + Ly::kA + st * kPBM * kPBK * 2, &tmA, leader_full, ks * kPBK, tm * kPBM, 0);
+            const uint32_t half = crank & 1, pair = crank >> 1;
+            tma_load_3d_pair_multicast(sm + Ly::kB + st * kBRows * kPBK * 2 + pair * (kBRows / 2) * kPBK * 2, &tmB,
+                                       leader_full, ks * kPBK,
+                                       tn * kPBN + static_cast<int>(half) * kBRows + static_cast<int>(pair) * (kBRows / 2),
+                                       0, static_cast<uint16_t>((1u << half) | (1u << (2 + half))), pol_w);
+          } else if constexpr (kPair) {
             // both CTAs' A and W halves complete on the leader's full barrier
             const uint32_t leader_full = mapa_u32(smem_u32(bar_full + st), 0);
             if (crank == 0) mbar_expect_tx(bar_full + st, 2 * (kPBM + kBRows) * kPBK * 2);
@@ -312,7 +333,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       });
     }
     __syncwarp();
-  } else if (warp == 1 && (!kPair || crank == 0)) {
+  } else if (warp == 1 && (!kPair || (crank & 1) == 0)) {
     constexpr uint32_t kId = idesc_bf16(kPair ? 2 * kPBM : kPBM, kPBN, 0, 0);
     if (elect_one()) {
       int it = 0, lt = 0;
@@ -336,13 +357,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
               mma_ss(acc, sdesc_sw128(ab + kk * 32, 16, 1024), sdesc_sw128(bb + kk * 32, 16, 1024), kId,
                      (ks > 0 || kk > 0) ? 1u : 0u);
           }
-          if constexpr (kPair)
+          if constexpr (kQuad)
+            tc_commit_pair(bar_empty + st, 0xF);  // every CTA's W quarter fed both pairs
+          else if constexpr (kPair)
             tc_commit_pair(bar_empty + st, 0x3);
           else
             tc_commit_multicast(bar_empty + st, 0x3);
         }
         if constexpr (kPair)
-          tc_commit_pair(bar_acc + buf, 0x3);
+          tc_commit_pair(bar_acc + buf, static_cast<uint16_t>(0x3u << lead));
         else
           tc_commit(bar_acc + buf);
         ++lt;
@@ -376,8 +399,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         if (hc == kPBN / 128 - 1) {
           tc_fence_before();
-          if (kPair && crank != 0)
-            mbar_arrive_cluster(mapa_u32(smem_u32(bar_accf + buf), 0));
+          if (kPair && (crank & 1) != 0)
+            mbar_arrive_cluster(mapa_u32(smem_u32(bar_accf + buf), lead));
           else
             mbar_arrive(bar_accf + buf);
         }
@@ -640,15 +663,21 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   int rc;
   CUtensorMap ma, mb;
   if ((rc = make_tmap_bf16_3d(&ma, x, chan, rows, 1, chan, kPBM)) != kOk) return rc;
-  if ((rc = make_tmap_bf16_3d(&mb, w_t, chan, n, 1, chan, kPBN / 2)) != kOk) return rc;  // W half
+  // W half per CTA; quad clusters load it as two multicast quarters
+  static const bool quad_map = env_int("OSP_PROJ_QUAD", 0) != 0 && env_int("OSP_PROJ_PAIR", 1) != 0 &&
+                               env_int("OSP_PROJ_DYN", 1) != 0;
+  if ((rc = make_tmap_bf16_3d(&mb, w_t, chan, n, 1, chan, quad_map ? kPBN / 4 : kPBN / 2)) != kOk) return rc;
   CUtensorMap mo;
   if ((rc = make_tmap_bf16_3d(&mo, out, n, rows, 1, out_stride, 32)) != kOk) return rc;  // epilogue boxes
-  static std::atomic<uint64_t> attr_done_1{0}, attr_done_2{0};
+  static std::atomic<uint64_t> attr_done_1{0}, attr_done_2{0}, attr_done_4{0};
   rc = set_smem_attr(reinterpret_cast<const void*>(qkv_gemm_kernel<false>), ProjLayout::kSmem, attr_done_1,
                      "cudaFuncSetAttribute(qkv_gemm)");
   if (rc != kOk) return rc;
   rc = set_smem_attr(reinterpret_cast<const void*>(qkv_gemm_kernel<true>), Proj2Layout::kSmem, attr_done_2,
                      "cudaFuncSetAttribute(qkv_gemm pair)");
+  if (rc != kOk) return rc;
+  rc = set_smem_attr(reinterpret_cast<const void*>(qkv_gemm_kernel<true, true>), Proj2Layout::kSmem, attr_done_4,
+                     "cudaFuncSetAttribute(qkv_gemm quad)");
   if (rc != kOk) return rc;
   // bands of 12 (measured best at cfg3, tools/bench_proj.py); column bands (the band's W slice
   // stays L2-resident while x streams): at cfg3 8.9 GB of DRAM reads per launch instead of 13.5
@@ -656,6 +685,8 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   static const int band = env_int("OSP_PROJ_BAND", 12);
   static const int col_bands = env_int("OSP_PROJ_ORDER", 1);
   static const bool pair = env_int("OSP_PROJ_PAIR", 1) != 0;
+  // two pairs per cluster sharing the W slice (needs the dynamic schedule)
+  static const bool quad_env = env_int("OSP_PROJ_QUAD", 0) != 0;
   a.band = band < 1 ? 12 : band;
   a.col_bands = col_bands;
   if (norm == 2) {
@@ -665,7 +696,9 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int n_units = a.n_pairs_m * a.n_tiles_n;
+  const bool quad = pair && quad_env && env_int("OSP_PROJ_DYN", 1) != 0;
+  const int ctas = quad ? 4 : 2;
+  const int n_units = (quad ? (a.n_pairs_m + 1) / 2 : a.n_pairs_m) * a.n_tiles_n;
   // dynamic unit schedule (pair kernel): a work counter zeroed on the stream before the launch;
   // launches rotate through 64 counters per device, so concurrent launches on other streams do
   // not share one
@@ -692,19 +725,20 @@ int launch_qkv_project(const void* x, const void* w_t, void* out, int64_t rows, 
       return rc;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * min(n_units, sms / 2));
+  cfg.gridDim = dim3(ctas * min(n_units, sms / ctas));
   cfg.blockDim = dim3(kPThreads);
   cfg.dynamicSmemBytes = pair ? Proj2Layout::kSmem : ProjLayout::kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = ctas;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  rc = check_cuda(pair ? cudaLaunchKernelEx(&cfg, qkv_gemm_kernel<true>, ma, mb, mo, a)
-                       : cudaLaunchKernelEx(&cfg, qkv_gemm_kernel<false>, ma, mb, mo, a),
+  rc = check_cuda(quad   ? cudaLaunchKernelEx(&cfg, qkv_gemm_kernel<true, true>, ma, mb, mo, a)
+                  : pair ? cudaLaunchKernelEx(&cfg, qkv_gemm_kernel<true>, ma, mb, mo, a)
+                         : cudaLaunchKernelEx(&cfg, qkv_gemm_kernel<false>, ma, mb, mo, a),
                   "qkv_gemm launch");
   if (rc != kOk || norm != 2) return rc;
   const int64_t warps = rows * 2;
